@@ -1,0 +1,72 @@
+"""Genome tensor layout (reference genome.py:1-115).
+
+A genome is the reference's pair of NaN-padded float64 tensors: nodes
+(max_nodes, 5) = (key, bias, response, aggregation_id, activation_id) and
+conns (max_conns, 4) = (in_key, out_key, enabled, weight).  The device keeps
+exactly this layout (float64, array-of-structs rows) so populations cross the
+host/device boundary without conversion and every attribute stays the
+reference's float64 value; the kernels read rows with 8/16-byte loads.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+NODE_KEY, NODE_BIAS, NODE_RESPONSE, NODE_AGG, NODE_ACT = range(5)
+CONN_IN, CONN_OUT, CONN_ENABLED, CONN_WEIGHT = range(4)
+NODE_ATTRS, CONN_ATTRS = 4, 2
+
+
+@dataclass(frozen=True, eq=False)
+class GenomeTensors:
+    """One genome (genome.py:65-79)."""
+    nodes: np.ndarray
+    conns: np.ndarray
+    num_inputs: int
+    num_outputs: int
+
+    @property
+    def max_nodes(self) -> int:
+        return self.nodes.shape[0]
+
+    @property
+    def max_conns(self) -> int:
+        return self.conns.shape[0]
+
+
+@dataclass(eq=False)
+class PopulationTensors:
+    """Stacked genomes plus bookkeeping (genome.py:82-115).  ``nodes`` and
+    ``conns`` may be numpy arrays or CUDA tensors (device-resident runs)."""
+    nodes: object
+    conns: object
+    species_id: np.ndarray
+    fitness: np.ndarray
+    num_inputs: int
+    num_outputs: int
+
+    @property
+    def size(self) -> int:
+        return int(self.nodes.shape[0])
+
+    def genome(self, index: int) -> GenomeTensors:
+        n, c = self.nodes[index], self.conns[index]
+        if not isinstance(n, np.ndarray):
+            n, c = n.cpu().numpy(), c.cpu().numpy()
+        return GenomeTensors(np.array(n, copy=True), np.array(c, copy=True),
+                             self.num_inputs, self.num_outputs)
+
+    @classmethod
+    def from_genomes(cls, genomes: list) -> "PopulationTensors":
+        if not genomes:
+            raise ValueError("population must be non-empty")
+        g0 = genomes[0]
+        for g in genomes[1:]:
+            if (g.nodes.shape, g.conns.shape, g.num_inputs, g.num_outputs) != \
+                    (g0.nodes.shape, g0.conns.shape, g0.num_inputs, g0.num_outputs):
+                raise ValueError("genomes disagree on tensor shapes or I/O counts")
+        k = len(genomes)
+        return cls(np.stack([g.nodes for g in genomes]), np.stack([g.conns for g in genomes]),
+                   np.full(k, -1, dtype=np.int64), np.full(k, np.nan), g0.num_inputs, g0.num_outputs)

@@ -1,0 +1,431 @@
+"""Two-phase inference on the GPU: transform (K1) and population forward (K2).
+
+Drop-in for reference inference.py:
+  * ``transform_arrays`` (inference.py:82-147)  -> csrc/transform.cu ``an_transform``
+  * ``forward_arrays``   (inference.py:185-262) -> csrc/forward.cu  ``an_forward``
+  * wrappers ``transform``, ``population_transform``,
+    ``transform_population_stacked``, ``forward``, ``forward_batch``,
+    ``population_forward`` (inference.py:150-319) with the same argument
+    checks and exceptions.
+
+``StackedNetworks`` duck-types the reference's (``size``, ``order``,
+``nodes``, ``incoming``, ``input_rows``, ``output_rows``, ``genome_view``) but
+its payload is the device-resident compiled program of every genome; the dense
+``incoming`` tensor is only materialised (lazily, on the host) if asked for.
+
+Precision: ``precision="f32"`` (default) evaluates in float32 -- the north-star
+path, parity ``|d| <= 1e-5 * max(1, |ref|)`` against the float64 reference;
+``precision="f64"`` evaluates in float64 for reference-exact checking
+(<= 1e-9 like the reference's own oracle tests, test_oracle.py:82-92).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native
+from .device import device, ptr, stream_handle, to_device
+from .errors import ConfigError, CycleDetected, IntegrityError, InvalidInput
+from .functions import DEFAULT_REGISTRY, check_registry
+
+ST_CYCLIC, ST_BAD_ACT, ST_BAD_AGG, ST_BAD_KEY, ST_DANGLING, ST_MISSING_IO = 1, 2, 4, 8, 16, 32
+_PREC = {"f32": 0, "f64": 1}
+_TORCH_DT = {0: torch.float32, 1: torch.float64}
+
+
+def _precision_code(precision) -> int:
+    if precision in _PREC:
+        return _PREC[precision]
+    raise ValueError(f"precision must be 'f32' or 'f64', got {precision!r}")
+
+
+@dataclass(eq=False)
+class StackedNetworks:
+    """Transformed population: compiled per-genome programs on the device."""
+
+    nodes_dev: torch.Tensor          # (P, N, 5) float64
+    conns_dev: torch.Tensor          # (P, C, 4) float64
+    num_inputs: int
+    num_outputs: int
+    program: torch.Tensor            # (P, stride) uint8
+    order_dev: torch.Tensor          # (P, N) int16, -1 padded
+    conn_rows: torch.Tensor          # (P, C, 2) int16
+    io_rows: torch.Tensor            # (P, I+O) int32
+    status_dev: torch.Tensor         # (P,) int32
+    maxdims: tuple[int, int, int]    # max (slots, steps, edges) over the population
+    precision: int = 0
+    mode: int = 0
+    _cache: dict = field(default_factory=dict, repr=False)
+
+    # -- reference duck-typing (inference.py:46-75) ----------------------------
+    @property
+    def size(self) -> int:
+        return int(self.program.shape[0])
+
+    @property
+    def max_nodes(self) -> int:
+        return int(self.nodes_dev.shape[1])
+
+    @property
+    def max_conns(self) -> int:
+        return int(self.conns_dev.shape[1])
+
+    @property
+    def stride(self) -> int:
+        return int(self.program.shape[1])
+
+    @property
+    def status(self) -> np.ndarray:
+        if "status" not in self._cache:
+            self._cache["status"] = self.status_dev.cpu().numpy()
+        return self._cache["status"]
+
+    @property
+    def nodes(self) -> np.ndarray:
+        if "nodes" not in self._cache:
+            self._cache["nodes"] = self.nodes_dev.cpu().numpy()
+        return self._cache["nodes"]
+
+    @property
+    def order(self) -> np.ndarray:
+        """(P, N) float64 row order, NaN padded (inference.py:125,133)."""
+        if "order" not in self._cache:
+            o = self.order_dev.to(torch.float64)
+            o[o < 0] = float("nan")
+            self._cache["order"] = o.cpu().numpy()
+        return self._cache["order"]
+
+    @property
+    def input_rows(self) -> np.ndarray:
+        return self.io_rows[:, : self.num_inputs].cpu().numpy().astype(np.int64)
+
+    @property
+    def output_rows(self) -> np.ndarray:
+        return self.io_rows[:, self.num_inputs:].cpu().numpy().astype(np.int64)
+
+    @property
+    def incoming(self) -> np.ndarray:
+        """(P, N, N) float64, incoming[p, dst, src] = weight, NaN where no
+        enabled edge (inference.py:108-112).  Materialised on demand."""
+        if "incoming" not in self._cache:
+            p, n = self.size, self.max_nodes
+            inc = torch.full((p, n, n), float("nan"), dtype=torch.float64, device=self.program.device)
+            rows = self.conn_rows.to(torch.int64)
+            pm, cm = torch.nonzero(rows[:, :, 0] >= 0, as_tuple=True)
+            inc[pm, rows[pm, cm, 1], rows[pm, cm, 0]] = self.conns_dev[pm, cm, 3]
+            self._cache["incoming"] = inc.cpu().numpy()
+        return self._cache["incoming"]
+
+    def genome_view(self, i: int) -> "TransformedNetwork":
+        sub = self.select(slice(i, i + 1))
+        return TransformedNetwork(sub)
+
+    def select(self, idx) -> "StackedNetworks":
+        """Row subset (a view on the same device buffers where possible)."""
+        return StackedNetworks(self.nodes_dev[idx], self.conns_dev[idx], self.num_inputs,
+                               self.num_outputs, self.program[idx], self.order_dev[idx],
+                               self.conn_rows[idx], self.io_rows[idx], self.status_dev[idx],
+                               self.maxdims, self.precision, self.mode)
+
+    @classmethod
+    def from_networks(cls, networks: list) -> "StackedNetworks":
+        parts = [t.stacked if isinstance(t, TransformedNetwork) else t for t in networks]
+        first = parts[0]
+        md = tuple(max(p.maxdims[k] for p in parts) for k in range(3))
+        cat = lambda name: torch.cat([getattr(p, name) for p in parts])  # noqa: E731
+        return cls(cat("nodes_dev"), cat("conns_dev"), first.num_inputs, first.num_outputs,
+                   cat("program"), cat("order_dev"), cat("conn_rows"), cat("io_rows"),
+                   cat("status_dev"), md, first.precision, first.mode)
+
+
+class TransformedNetwork:
+    """Inference-ready single genome (inference.py:30-43) backed by a
+    one-genome StackedNetworks."""
+
+    def __init__(self, stacked: StackedNetworks):
+        self.stacked = stacked
+
+    @property
+    def nodes(self) -> np.ndarray:
+        return self.stacked.nodes[0]
+
+    @property
+    def order(self) -> np.ndarray:
+        return self.stacked.order[0]
+
+    @property
+    def conns_expanded(self) -> np.ndarray:
+        """(N, N, 1): [i, j, 0] = weight of the enabled edge row i -> row j."""
+        return self.stacked.incoming[0].T[:, :, None]
+
+    @property
+    def input_rows(self) -> np.ndarray:
+        return self.stacked.input_rows[0]
+
+    @property
+    def output_rows(self) -> np.ndarray:
+        return self.stacked.output_rows[0]
+
+
+# ---------------------------------------------------------------------------
+# transform
+# ---------------------------------------------------------------------------
+
+def transform_arrays(nodes, conns, num_inputs: int, num_outputs: int, *,
+                     precision: str = "f32", network_type: str = "feedforward",
+                     prune: bool = True, stream: torch.cuda.Stream | None = None,
+                     sync: bool = True) -> tuple[StackedNetworks, np.ndarray]:
+    """Kahn transform of every genome at once (inference.py:82-147).
+
+    Returns the stacked programs and the indices of cyclic genomes (their
+    programs are empty).  ``nodes``/``conns`` may be numpy or torch (any
+    device).  With ``sync=False`` the cyclic list and launch sizes are not
+    read back (the caller must call ``finalize_transform`` before forward).
+    """
+    prec = _precision_code(precision)
+    mode = {"feedforward": 0, "recurrent": 1}[network_type]
+    nd = to_device(nodes, torch.float64)
+    cd = to_device(conns, torch.float64)
+    if nd.dim() != 3 or nd.shape[2] != 5 or cd.dim() != 3 or cd.shape[2] != 4 or nd.shape[0] != cd.shape[0]:
+        raise ValueError(f"expected (P,N,5) and (P,C,4) tensors, got {tuple(nd.shape)}, {tuple(cd.shape)}")
+    pop, n, c = int(nd.shape[0]), int(nd.shape[1]), int(cd.shape[1])
+    stride = int(_native.lib().an_program_stride(n, c, num_outputs, prec))
+    dev = nd.device
+    program = torch.empty((pop, stride), dtype=torch.uint8, device=dev)
+    order = torch.empty((pop, n), dtype=torch.int16, device=dev)
+    conn_rows = torch.empty((pop, c, 2), dtype=torch.int16, device=dev)
+    io_rows = torch.empty((pop, num_inputs + num_outputs), dtype=torch.int32, device=dev)
+    status = torch.zeros((pop,), dtype=torch.int32, device=dev)
+    maxdims = torch.zeros((3,), dtype=torch.int32, device=dev)
+    _native.call("an_transform", ptr(nd), ptr(cd), pop, n, c, num_inputs, num_outputs, mode, prec,
+                 int(bool(prune)), ptr(program), stride, ptr(order), ptr(conn_rows), ptr(io_rows),
+                 ptr(status), ptr(maxdims), stream_handle(stream))
+    stacked = StackedNetworks(nd, cd, num_inputs, num_outputs, program, order, conn_rows, io_rows,
+                              status, (0, 0, 0), prec, mode)
+    stacked._cache["maxdims_dev"] = maxdims
+    if not sync:
+        return stacked, np.zeros(0, dtype=np.int64)
+    return stacked, finalize_transform(stacked)
+
+
+def finalize_transform(stacked: StackedNetworks) -> np.ndarray:
+    """Read back launch sizes and per-genome status; raise on invalid genomes;
+    return the cyclic genome indices (feed-forward mode)."""
+    md = stacked._cache.pop("maxdims_dev", None)
+    if md is not None:
+        stacked.maxdims = tuple(int(v) for v in md.cpu().tolist())
+    st = stacked.status
+    hard = st & (ST_BAD_KEY | ST_DANGLING | ST_MISSING_IO)
+    if hard.any():
+        bad = np.nonzero(hard)[0]
+        raise IntegrityError(f"genome tensors violate structural invariants at indices {bad[:20].tolist()} "
+                             f"(status bits {sorted(set(int(x) for x in st[bad[:20]]))})")
+    if stacked.mode == 1:
+        return np.zeros(0, dtype=np.int64)
+    return np.nonzero(st & ST_CYCLIC)[0].astype(np.int64)
+
+
+def _raise_cycles(cyclic: np.ndarray, offset: int = 0, msg: str | None = None) -> None:
+    if cyclic.size:
+        bad = (cyclic + offset).tolist()
+        raise CycleDetected(msg or f"enabled connections contain a directed cycle in genomes {bad}",
+                            genome_indices=bad)
+
+
+def _genome_parts(genome):
+    return genome.nodes[None], genome.conns[None], genome.num_inputs, genome.num_outputs
+
+
+def transform(genome, **kw) -> TransformedNetwork:
+    """One genome; raises CycleDetected on an enabled cycle (inference.py:150-158)."""
+    n, c, i, o = _genome_parts(genome)
+    stacked, cyclic = transform_arrays(n, c, i, o, **kw)
+    if cyclic.size:
+        raise CycleDetected("enabled connections contain a directed cycle")
+    return TransformedNetwork(stacked)
+
+
+def population_transform(pop, **kw) -> list[TransformedNetwork]:
+    """Every genome; aggregated CycleDetected (inference.py:161-168)."""
+    stacked = transform_population_stacked(pop, **kw)
+    return [stacked.genome_view(i) for i in range(stacked.size)]
+
+
+def transform_population_stacked(pop, **kw) -> StackedNetworks:
+    """Stacked variant used by the evolution loop (inference.py:171-178)."""
+    stacked, cyclic = transform_arrays(pop.nodes, pop.conns, pop.num_inputs, pop.num_outputs, **kw)
+    _raise_cycles(cyclic)
+    return stacked
+
+
+# ---------------------------------------------------------------------------
+# forward
+# ---------------------------------------------------------------------------
+
+def _check_codes(stacked: StackedNetworks) -> None:
+    st = stacked.status
+    if (st & ~ST_CYCLIC & (ST_BAD_ACT | ST_BAD_AGG)).any():
+        which = np.nonzero(st & (ST_BAD_ACT | ST_BAD_AGG))[0][:10].tolist()
+        kind = "activation" if (st & ST_BAD_ACT).any() else "aggregation"
+        raise ConfigError(f"unknown {kind} code in genomes {which}")
+
+
+def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Tensor | None = None,
+                   *, shared: bool = False, variant: int = 0,
+                   stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Device-resident forward: inputs (P,B,I) (or (B,I) with shared=True) on
+    the GPU in the program's dtype -> outputs (P,B,O).  No host syncs."""
+    dt = _TORCH_DT[stacked.precision]
+    if inputs.dtype != dt or not inputs.is_cuda or not inputs.is_contiguous():
+        raise ValueError(f"inputs must be a contiguous CUDA {dt} tensor")
+    pop = stacked.size
+    if shared:
+        b, i = int(inputs.shape[-2]), int(inputs.shape[-1])
+        gstride = 0
+    else:
+        if inputs.dim() != 3 or inputs.shape[0] != pop:
+            raise ValueError(f"expected inputs of shape (P={pop}, B, I), got {tuple(inputs.shape)}")
+        b, i = int(inputs.shape[1]), int(inputs.shape[2])
+        gstride = b * i
+    if i != stacked.num_inputs:
+        raise InvalidInput(f"expected input length {stacked.num_inputs}, got {i}")
+    if out is None:
+        out = torch.empty((pop, b, stacked.num_outputs), dtype=dt, device=inputs.device)
+    md = _maxdims_arg(stacked)
+    _native.call("an_forward", ptr(stacked.program), stacked.stride, stacked.max_nodes,
+                 stacked.max_conns, stacked.precision, md, ptr(inputs), gstride, pop, b, i,
+                 stacked.num_outputs, ptr(out), int(variant), stream_handle(stream))
+    return out
+
+
+def _maxdims_arg(stacked: StackedNetworks) -> int:
+    """Host int32[3] launch sizes, kept alive on the stacked object."""
+    arr = stacked._cache.get("maxdims_host")
+    if arr is None or tuple(arr) != tuple(stacked.maxdims):
+        arr = (ctypes.c_int32 * 3)(*[int(v) for v in stacked.maxdims])
+        stacked._cache["maxdims_host"] = arr
+    return ctypes.addressof(arr)
+
+
+def _host_forward_pipelined(stacked: StackedNetworks, x: torch.Tensor, out_host: torch.Tensor,
+                            chunk_bytes: int = 256 << 20, variant: int = 0) -> torch.Tensor:
+    """Host (P,B,I) -> host (P,B,O) in genome chunks: H2D copy of chunk k+1
+    and D2H of chunk k-1 overlap the kernel on chunk k (two copy streams,
+    double-buffered device staging).  Pinned host tensors make the copies
+    asynchronous DMA."""
+    pop, b, i = x.shape
+    o = stacked.num_outputs
+    dt = _TORCH_DT[stacked.precision]
+    dev = device()
+    per = max(1, int(chunk_bytes // max(1, b * i * x.element_size())))
+    bufs_in = [torch.empty((min(per, pop), b, i), dtype=dt, device=dev) for _ in range(2)]
+    bufs_out = [torch.empty((min(per, pop), b, o), dtype=dt, device=dev) for _ in range(2)]
+    h2d, comp, d2h = torch.cuda.Stream(), torch.cuda.current_stream(), torch.cuda.Stream()
+    in_free = [None, None]
+    out_free = [None, None]
+    for k, lo in enumerate(range(0, pop, per)):
+        hi = min(pop, lo + per)
+        slot = k & 1
+        with torch.cuda.stream(h2d):
+            if in_free[slot] is not None:
+                h2d.wait_event(in_free[slot])
+            dst = bufs_in[slot][: hi - lo]
+            dst.copy_(x[lo:hi], non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(h2d)
+        comp.wait_event(ready)
+        if out_free[slot] is not None:
+            comp.wait_event(out_free[slot])
+        forward_device(stacked.select(slice(lo, hi)), dst, bufs_out[slot][: hi - lo],
+                       variant=variant, stream=comp)
+        done = torch.cuda.Event()
+        done.record(comp)
+        in_free[slot] = done
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(done)
+            out_host[lo:hi].copy_(bufs_out[slot][: hi - lo], non_blocking=True)
+            fin = torch.cuda.Event()
+            fin.record(d2h)
+        out_free[slot] = fin
+    d2h.synchronize()
+    return out_host
+
+
+def forward_arrays(stacked: StackedNetworks, registry=None, inputs=None, *, variant: int = 0,
+                   out=None):
+    """Batched forward, inputs (P, B, I) -> outputs (P, B, O) (inference.py:185-262).
+
+    numpy inputs -> numpy float64 outputs (reference behaviour); torch CUDA
+    inputs -> torch outputs on the device; torch CPU inputs (ideally pinned)
+    -> torch CPU outputs through the chunked copy/compute pipeline.
+    """
+    check_registry(registry)
+    _check_codes(stacked)
+    dt = _TORCH_DT[stacked.precision]
+    if isinstance(inputs, torch.Tensor) and inputs.is_cuda:
+        x = inputs if inputs.dtype == dt else inputs.to(dt)
+        return forward_device(stacked, x.contiguous(), out, variant=variant)
+    if isinstance(inputs, torch.Tensor):
+        x = inputs if inputs.dtype == dt else inputs.to(dt)
+        if out is None:
+            out = torch.empty((x.shape[0], x.shape[1], stacked.num_outputs), dtype=dt,
+                              pin_memory=x.is_pinned())
+        return _host_forward_pipelined(stacked, x.contiguous(), out, variant=variant)
+    arr = np.asarray(inputs)
+    if arr.ndim == 3 and arr.strides[0] == 0:
+        # broadcast_to inputs shared by every genome (problems.py:230,253)
+        shared = to_device(arr[0], dt)
+        return forward_device(stacked, shared, shared=True, variant=variant).cpu().numpy().astype(np.float64)
+    x = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32 if dt == torch.float32 else np.float64))
+    res = torch.empty((x.shape[0], x.shape[1], stacked.num_outputs), dtype=dt)
+    if x.numel() * x.element_size() <= (64 << 20):
+        res = forward_device(stacked, to_device(x, dt), variant=variant).cpu()
+    else:
+        res = _host_forward_pipelined(stacked, x, res, variant=variant)
+    return res.numpy().astype(np.float64)
+
+
+def _check_inputs(arr: np.ndarray, num_inputs: int) -> None:
+    """inference.py:265-269."""
+    if arr.shape[-1] != num_inputs:
+        raise InvalidInput(f"expected input length {num_inputs}, got {arr.shape[-1]}")
+    if np.isnan(arr).any():
+        raise InvalidInput("input contains NaN")
+
+
+def forward(tn: TransformedNetwork, registry=None, inputs=None) -> np.ndarray:
+    """(I,) -> (O,) (inference.py:279-287)."""
+    arr = np.asarray(inputs, dtype=np.float64)
+    if arr.ndim != 1:
+        raise InvalidInput(f"expected a 1-D input vector, got shape {arr.shape}")
+    _check_inputs(arr, tn.stacked.num_inputs)
+    return forward_arrays(tn.stacked, registry or DEFAULT_REGISTRY, arr[None, None, :])[0, 0]
+
+
+def forward_batch(tn: TransformedNetwork, registry=None, inputs=None) -> np.ndarray:
+    """(B, I) -> (B, O) (inference.py:290-300)."""
+    arr = np.asarray(inputs, dtype=np.float64)
+    if arr.ndim != 2:
+        raise InvalidInput(f"expected a (B, I) input matrix, got shape {arr.shape}")
+    if arr.shape[0] < 1:
+        raise InvalidInput("batch must contain at least one row")
+    _check_inputs(arr, tn.stacked.num_inputs)
+    return forward_arrays(tn.stacked, registry or DEFAULT_REGISTRY, arr[None])[0]
+
+
+def population_forward(transformed, registry=None, inputs=None) -> np.ndarray:
+    """(P, I) or (P, B, I) -> per-genome outputs (inference.py:303-319)."""
+    stacked = transformed if isinstance(transformed, StackedNetworks) \
+        else StackedNetworks.from_networks(list(transformed))
+    arr = np.asarray(inputs, dtype=np.float64)
+    if arr.ndim == 2:
+        _check_inputs(arr, stacked.num_inputs)
+        return forward_arrays(stacked, registry or DEFAULT_REGISTRY, arr[:, None, :])[:, 0, :]
+    if arr.ndim == 3:
+        _check_inputs(arr, stacked.num_inputs)
+        return forward_arrays(stacked, registry or DEFAULT_REGISTRY, arr)
+    raise InvalidInput(f"expected (P, I) or (P, B, I) inputs, got shape {arr.shape}")

@@ -1,0 +1,134 @@
+"""GPU parity: transform (K1) and forward (K2) against the reference goldens
+and the oracle.  Calls go through the package -> ctypes -> C ABI.
+
+Tolerances (written here, per north_star):
+  * transform order / io rows / dense incoming / cyclic list: bit-exact;
+  * f64 programs: |d| <= 1e-9 (the reference's own oracle bound, test_oracle.py:82-92);
+  * f32 programs: |d| <= 1e-5 * max(1, |ref|) on the tanh/sum
+    north-star networks; mixed act/agg networks (identity/product chains
+    amplify fp32 rounding) use 1e-4 * max(1, |ref|).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import cuda_ok, load_golden
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["forward_small.npz", "forward_cfg2_T.npz", "forward_cfg2_M.npz", "corpus.npz"]
+
+
+@pytest.fixture(scope="module")
+def tn():
+    if not cuda_ok():
+        pytest.skip("no CUDA device")
+    import paper_2404_01817_b200 as tn
+    return tn
+
+
+def _rel_err(out, ref):
+    return np.max(np.abs(out - ref) / np.maximum(1.0, np.abs(ref)))
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_transform_bit_exact(tn, name, precision):
+    g = load_golden(name)
+    st, cyc = tn.transform_arrays(g["nodes"], g["conns"], int(g["num_inputs"]),
+                                  int(g["num_outputs"]), precision=precision)
+    assert np.array_equal(cyc, g["cyclic"])
+    assert np.array_equal(st.order, g["order"], equal_nan=True)
+    ok = np.setdiff1d(np.arange(g["nodes"].shape[0]), g["cyclic"])
+    assert np.array_equal(st.input_rows[ok], g["input_rows"][ok])
+    assert np.array_equal(st.output_rows[ok], g["output_rows"][ok])
+    if "incoming" in g:
+        assert np.array_equal(st.incoming, g["incoming"], equal_nan=True)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_forward_f64_matches_reference(tn, name):
+    g = load_golden(name)
+    ok = np.setdiff1d(np.arange(g["nodes"].shape[0]), g["cyclic"])
+    st, cyc = tn.transform_arrays(g["nodes"][ok], g["conns"][ok], int(g["num_inputs"]),
+                                  int(g["num_outputs"]), precision="f64")
+    assert cyc.size == 0
+    out = tn.forward_arrays(st, None, g["inputs"][ok])
+    np.testing.assert_allclose(out, g["outputs"][ok], rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.parametrize("name,tol", [("forward_cfg2_T.npz", 1e-5), ("forward_small.npz", 1e-4),
+                                      ("forward_cfg2_M.npz", 1e-4), ("corpus.npz", 1e-4)])
+def test_forward_f32_matches_reference(tn, name, tol):
+    g = load_golden(name)
+    ok = np.setdiff1d(np.arange(g["nodes"].shape[0]), g["cyclic"])
+    st, _ = tn.transform_arrays(g["nodes"][ok], g["conns"][ok], int(g["num_inputs"]),
+                                int(g["num_outputs"]))
+    x = g["inputs_f32"][ok] if "inputs_f32" in g else g["inputs"][ok].astype(np.float32)
+    ref = g["outputs"][ok]
+    for variant in (0, 1, 2, 4, 8):
+        out = tn.forward_arrays(st, None, x, variant=variant)
+        assert _rel_err(out, ref) <= tol, (variant, _rel_err(out, ref))
+
+
+def test_tile_variants_bitwise_equal_and_chunk_invariant(tn):
+    import torch
+    from oracle.arrayneat_oracle import synthetic_population
+    nodes, conns = synthetic_population(40, 128, 512, 32, 8, seed=77)
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8)
+    x = torch.randn(40, 1000, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
+    outs = [tn.forward_device(st, x, variant=v) for v in (1, 2, 4)]
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+    # genome chunks and input chunks give bitwise identical results
+    part = torch.cat([tn.forward_device(st.select(slice(a, a + 13)), x[a:a + 13].contiguous(), variant=2)
+                      for a in range(0, 40, 13)])
+    assert torch.equal(part, outs[1])
+    half = tn.forward_device(st, x[:, 300:700].contiguous(), variant=2)
+    assert torch.equal(half, outs[1][:, 300:700])
+
+
+def test_config2_shapes_against_oracle_sampled(tn):
+    """Full config-2 genome shapes and B=4096; a sampled set of genomes is
+    checked against the oracle (float64) within the fp32 bound."""
+    import torch
+    from oracle import arrayneat_oracle as orc
+    nodes, conns = orc.synthetic_population(64, 128, 512, 32, 8, seed=20261018)
+    st, cyc = tn.transform_arrays(nodes, conns, 32, 8)
+    assert cyc.size == 0
+    x = np.random.default_rng(20261019).standard_normal((64, 4096, 32), dtype=np.float32)
+    out = tn.forward_device(st, torch.from_numpy(x).cuda()).cpu().numpy()
+    for p in (0, 17, 63):
+        tr = orc.transform_genome(nodes[p], conns[p], 32, 8)
+        ref = orc.forward_genome(nodes[p], tr, x[p].astype(np.float64))
+        assert _rel_err(out[p], ref) <= 1e-5
+
+
+def test_cycle_and_errors(tn):
+    g = load_golden("forward_small.npz")
+    with pytest.raises(tn.CycleDetected) as exc:
+        tn.transform_population_stacked(
+            tn.PopulationTensors(g["nodes"], g["conns"], None, None, 2, 1))
+    assert exc.value.genome_indices == [47]
+    nodes = g["nodes"][:2].copy()
+    nodes[0, 2, 4] = 9.0  # unknown activation code on a live node
+    st, _ = tn.transform_arrays(nodes, g["conns"][:2], 2, 1)
+    if not np.isnan(nodes[0, 2, 0]):
+        with pytest.raises(tn.ConfigError):
+            tn.forward_arrays(st, None, np.zeros((2, 1, 2)))
+
+
+def test_single_genome_wrappers(tn):
+    g = load_golden("forward_small.npz")
+    from paper_2404_01817_b200.genome import GenomeTensors
+    genome = GenomeTensors(g["nodes"][3], g["conns"][3], 2, 1)
+    t = tn.transform(genome, precision="f64")
+    y = tn.forward(t, None, g["inputs"][3][0])
+    np.testing.assert_allclose(y, g["outputs"][3][0], atol=1e-9)
+    yb = tn.forward_batch(t, None, g["inputs"][3])
+    np.testing.assert_allclose(yb, g["outputs"][3], atol=1e-9)
+    with pytest.raises(tn.InvalidInput):
+        tn.forward(t, None, [1.0, np.nan])
+    with pytest.raises(tn.InvalidInput):
+        tn.forward(t, None, [1.0, 2.0, 3.0])
