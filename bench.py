@@ -268,8 +268,9 @@ def run_ours(args, rank: int, world: int) -> None:
     value = evals / elapsed
 
     # algorithmic bytes of one forward launch: inputs + outputs + each genome's program once
-    hdr = st.program[:, :8].contiguous().view(torch.int32)[:, :2].to(torch.int64).cpu().numpy()
-    prog_bytes = int((32 + 16 + 16 * hdr[:, 0] + 8 * hdr[:, 1]).sum())
+    hdr = st.program[:, :32].contiguous().view(torch.int32).to(torch.int64).cpu().numpy()
+    # header + output slots + groups + steps + edge entries (common.cuh layout)
+    prog_bytes = int((32 + 16 + 16 * hdr[:, 7] + 16 * hdr[:, 0] + 6 * hdr[:, 1]).sum())
     algo_bytes = pop * BATCH * 4 * (NIN + NOUT) + prog_bytes
     fwd_avg = statistics.mean(fwd_ms) / 1e3
     peak, peak_kind = _peaks()

@@ -61,12 +61,18 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
  *            input_genome_stride = elements between genomes (0 = shared inputs,
  *            as XorProblem.evaluate_stacked broadcasts them, problems.py:230)
  *   outputs  (P, B, O), same dtype
- *   maxdims_host  HOST pointer to the 3 ints an_transform produced
- *   variant  0 auto, 1/2/4 = tile kernel with 1/2/4 inputs per thread,
+ *   maxdims_host  HOST pointer to 3 ints {value slots, steps, edge entries}:
+ *            the an_transform maxima, or tighter bounds for the genomes listed
+ *   genome_ids  optional (P,) int32 DEVICE list of program rows to evaluate
+ *            (NULL = rows 0..P-1); inputs/outputs are addressed by program row,
+ *            so a launch per slot-count bucket raises occupancy
+ *   variant  0 auto, 1/3 = tile kernel 1 input/thread (128/64 threads),
+ *            2/5 = 2 inputs/thread (128/64 threads), 4 = 4 inputs/thread,
  *            8 = warp-per-genome kernel (small B) */
 int an_forward(const void* program, int64_t program_stride, int N, int C, int precision,
-               const int32_t* maxdims_host, const void* inputs, int64_t input_genome_stride,
-               int64_t P, int B, int I, int O, void* outputs, int variant, void* stream);
+               const int32_t* maxdims_host, const int32_t* genome_ids, const void* inputs,
+               int64_t input_genome_stride, int64_t P, int B, int I, int O, void* outputs, int variant,
+               void* stream);
 
 /* Forward fused with the built-in fitness.  Replaces
  * XorProblem.evaluate_stacked (problems.py:229-231, fitness :54-56) for

@@ -4,15 +4,16 @@
 // into a fixed-stride "program" that the forward kernels (forward.cu) execute.
 // A program is a flat byte block per genome:
 //
-//   [ProgHeader 32 B][out_slot u16 x O, padded to 16 B][Step x N][Edge x C]
+//   [ProgHeader 32 B][out_slot u16 x O][GroupRec x N][Step x N][edges x (3C+8N+16)]
 //
-// Steps are the non-input nodes in the reference's Kahn order
-// (inference.py:127-141) that can influence an output (ancestor-cone pruning,
-// SURVEY.md App. B "K2 ... safe optimisation"); edges are the enabled incoming
-// connections of each step, sorted by source row (inference.py:108-112 keeps a
-// dense incoming row; we keep its non-NaN entries in the same column order).
-// "Slots" index node values: slot i < I is input key i, later slots hold the
-// stored steps in order.
+// Steps are the non-input nodes that can influence an output (ancestor-cone
+// pruning, SURVEY.md App. B "K2 ... safe optimisation"), ordered by
+// topological level (a valid topological order; node values do not depend on
+// the evaluation order of independent nodes, so this is exact) and grouped.
+// Each step's edges are its enabled incoming connections in source-row order
+// (the non-NaN entries of the reference's dense incoming row,
+// inference.py:108-112).  "Slots" index node values: slot i < I starts as
+// input key i; slots are recycled once their last reader has run (liveness).
 #pragma once
 
 #include <cstdint>
@@ -38,47 +39,82 @@ constexpr uint16_t NO_SLOT = 0xFFFF;
 
 struct ProgHeader {  // 32 bytes
   int32_t n_steps;   // evaluated (non-input, needed) nodes
-  int32_t n_edges;   // edges referenced by the steps
+  int32_t n_edges;   // edge entries, including padding
   int32_t n_slots;   // value slots (inputs first)
   int32_t n_order;   // nodes placed in the Kahn order
   int32_t status;    // ST_* bits
   int32_t n_live;    // live node rows
   int32_t mode;      // 0 feed-forward, 1 recurrent
-  int32_t reserved;
+  int32_t n_groups;  // step groups
 };
 
+// A group is 1..4 steps of the same topological level (no edges between them)
+// with the same aggregation class.  Their edge lists are interleaved
+// round-major with a row width of gw = (n == 3 ? 4 : n) entries -- edge r of
+// step j sits at e_begin + r*gw + j -- so the forward kernel accumulates the n
+// nodes in lock-step as n independent FMA chains; entries past a step's count
+// are holes, skipped by a (warp-uniform) predicate.  e_begin is a multiple of
+// 8, so two rounds of sources / weights are single 16-byte loads.  Non-sum
+// aggregations are singleton groups.
+struct __align__(16) GroupRec {  // 16 bytes
+  uint8_t n;           // steps in the group (1..4)
+  uint8_t cls;         // GRP_* bits: GRP_GENERIC = non-sum aggregation (singleton),
+                       // GRP_TANH_SUM = every step is tanh/sum (fast epilogue)
+  uint16_t rounds;     // longest edge list in the group
+  uint16_t e_begin;    // first edge entry (multiple of 8)
+  uint16_t step_begin;
+  uint16_t cnt[4];     // edge count of each step
+};
+
+enum : uint8_t { GRP_GENERIC = 1, GRP_TANH_SUM = 2 };
+
+__host__ __device__ inline int group_width(int n) { return n == 3 ? 4 : n; }
+
 template <typename T> struct StepT;
+// fp32 step: activation evaluated branch-free (common.cuh step_act)
 template <> struct __align__(16) StepT<float> {
-  uint16_t slot; uint8_t act; uint8_t agg; uint16_t e_begin; uint16_t e_count;
+  uint16_t slot; uint8_t act; uint8_t agg; uint16_t count; uint16_t pad;
   float bias; float resp;
 };
 template <> struct __align__(16) StepT<double> {
-  uint16_t slot; uint8_t act; uint8_t agg; uint16_t e_begin; uint16_t e_count;
-  uint32_t pad; double bias; double resp;
+  uint16_t slot; uint8_t act; uint8_t agg; uint16_t count; uint16_t pad;
+  uint64_t pad2; double bias; double resp;
 };
-template <typename T> struct EdgeT;
-template <> struct __align__(8) EdgeT<float> { uint32_t src; float w; };
-template <> struct __align__(16) EdgeT<double> { uint32_t src; uint32_t pad; double w; };
+// fp64 programs keep (source slot, weight) pairs; fp32 programs keep two
+// arrays, u16 source slots and f32 weights (6 bytes per edge)
+struct __align__(16) EdgeD { uint32_t src; uint32_t pad; double w; };
 
+static_assert(sizeof(GroupRec) == 16, "group layout");
 static_assert(sizeof(StepT<float>) == 16, "step layout");
 static_assert(sizeof(StepT<double>) == 32, "step layout");
-static_assert(sizeof(EdgeT<float>) == 8, "edge layout");
-static_assert(sizeof(EdgeT<double>) == 16, "edge layout");
+static_assert(sizeof(EdgeD) == 16, "edge layout");
 
 __host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+// edge entries a genome may need: each group's list is padded to gw*rounds
+// (a step joins a group only if its list is >= half the longest, so padded
+// <= 8/3 x real) and starts on a multiple of 8
+__host__ __device__ inline int64_t edge_capacity(int N, int C) { return 3ll * C + 8ll * N + 16; }
+
 struct ProgLayout {
-  int64_t off_out, off_steps, off_edges, stride;
+  int64_t off_out, off_groups, off_steps, off_src, off_w, stride;
 };
 
 __host__ __device__ inline ProgLayout prog_layout(int N, int C, int O, int precision) {
   ProgLayout L;
-  const int64_t ss = precision ? sizeof(StepT<double>) : sizeof(StepT<float>);
-  const int64_t es = precision ? sizeof(EdgeT<double>) : sizeof(EdgeT<float>);
-  L.off_out = sizeof(ProgHeader);
-  L.off_steps = align_up(L.off_out + 2 * (int64_t)O, 16);
-  L.off_edges = align_up(L.off_steps + ss * N, 16);
-  L.stride = align_up(L.off_edges + es * C, 16);
+  const int64_t E = edge_capacity(N, C);
+  L.off_out = 32;
+  L.off_groups = align_up(L.off_out + 2 * (int64_t)O, 16);
+  L.off_steps = align_up(L.off_groups + 16ll * N, 16);
+  if (precision) {
+    L.off_src = align_up(L.off_steps + 32ll * N, 16);
+    L.off_w = L.off_src;  // EdgeD pairs
+    L.stride = align_up(L.off_w + 16 * E, 16);
+  } else {
+    L.off_src = align_up(L.off_steps + 16ll * N, 16);
+    L.off_w = align_up(L.off_src + 2 * E, 16);
+    L.stride = align_up(L.off_w + 4 * E, 16);
+  }
   return L;
 }
 
@@ -107,6 +143,14 @@ __device__ __forceinline__ float tanh_fast(float x) {
 // sigmoid = exp(-logaddexp(0, -x)) = 1 / (1 + exp(-x))  (functions.py:20-22)
 __device__ __forceinline__ float sigmoid_fast(float x) {
   return rcp_approx(1.0f + ex2_approx(-1.4426950408889634f * x));
+}
+
+// branch-free fp32 activation of a step (see StepT<float>)
+__device__ __forceinline__ float step_act(float kx, float ca, float cb, bool relu, float pre) {
+  const float sg = rcp_approx(1.0f + ex2_approx(kx * pre));
+  const float smooth = fmaf(ca, sg, cb);
+  const float lin = relu ? fmaxf(pre, 0.0f) : pre;
+  return kx != 0.0f ? smooth : lin;
 }
 
 __device__ __forceinline__ float apply_act(int code, float x) {

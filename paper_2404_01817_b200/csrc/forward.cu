@@ -6,12 +6,16 @@
 //   * fwd_tile: one CTA per (genome, tile of NT*S inputs).  Each thread owns S
 //     consecutive inputs; node values live in shared memory as [slot][tile]
 //     (inputs first, staged from HBM with 16-byte loads), so a thread only ever
-//     reads values it wrote itself -- no barrier inside the node sweep.  Edge
-//     descriptors are warp-uniform broadcast reads, value reads are S-wide
-//     vector loads.  For large per-genome batches (config 2: B = 4096).
-//   * fwd_warp: one warp per genome; lanes split a node's incoming edges and
-//     combine with warp-shuffle reductions (sum/product/max/min/mean).  For
-//     small batches (XOR B=4, regression B=64, cart-pole B=1) where a
+//     reads values it wrote itself -- no barrier inside the node sweep.  Steps
+//     are executed a group at a time (<= 4 independent same-level nodes with
+//     interleaved edge lists): the group's nodes accumulate in lock-step as
+//     independent FMA chains, which is what hides shared-memory and MUFU latency
+//     at the occupancy the value tiles allow.  Edge descriptors are warp-uniform
+//     (uniform-register addressed) 16-byte loads, value reads S-wide vector loads.
+//     For large per-genome batches (config 2: B = 4096).
+//   * fwd_warp: one warp per (genome, input chunk); lanes split a node's incoming
+//     edges and combine with warp-shuffle reductions (sum/product/max/min/mean).
+//     For small batches (XOR B=4, regression B=64, cart-pole B=1) where a
 //     thread-per-input mapping would idle most lanes.  Optionally fuses the
 //     XOR / regression fitness epilogue (problems.py:54-61).
 //
@@ -25,143 +29,377 @@ namespace tneat {
 
 template <typename T, int S> struct __align__(sizeof(T) * S) Pack { T v[S]; };
 
-template <typename T, int S, int NT>
-__global__ void __launch_bounds__(NT) fwd_tile_kernel(const uint8_t* __restrict__ prog, ProgLayout L,
-                                                      const T* __restrict__ in, int64_t in_gstride,
-                                                      int B, int I, int O, int tiles,
-                                                      T* __restrict__ out, int64_t out_gstride) {
-  constexpr int TT = NT * S;
-  using PackT = Pack<T, S>;
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int64_t gi = blockIdx.x / tiles;
-  const int tile = (int)(blockIdx.x - gi * tiles);
-  const uint8_t* gp = prog + gi * L.stride;
-  const ProgHeader hdr = *reinterpret_cast<const ProgHeader*>(gp);
-  const int n_steps = hdr.n_steps, n_edges = hdr.n_edges;
-  const int tid = threadIdx.x;
-
-  StepT<T>* st_s = reinterpret_cast<StepT<T>*>(smem);
-  const int64_t off_e = align_up((int64_t)n_steps * sizeof(StepT<T>), 16);
-  EdgeT<T>* ed_s = reinterpret_cast<EdgeT<T>*>(smem + off_e);
-  const int64_t off_v = align_up(off_e + (int64_t)n_edges * sizeof(EdgeT<T>), 16);
-  T* vals = reinterpret_cast<T*>(smem + off_v);
-
-  // program -> shared memory (edge sources become byte offsets of the slot row)
-  {
-    const int4* src = reinterpret_cast<const int4*>(gp + L.off_steps);
-    int4* dst = reinterpret_cast<int4*>(st_s);
-    const int n16 = (int)((int64_t)n_steps * sizeof(StepT<T>) / 16);
-    for (int i = tid; i < n16; i += NT) dst[i] = __ldg(src + i);
-    const EdgeT<T>* esrc = reinterpret_cast<const EdgeT<T>*>(gp + L.off_edges);
-    for (int e = tid; e < n_edges; e += NT) {
-      EdgeT<T> x = esrc[e];
-      x.src = x.src * (uint32_t)(TT * sizeof(T));
-      ed_s[e] = x;
-    }
-  }
-
-  // inputs -> value slots 0..I-1 (input key i lives in slot i)
-  const int s0 = tile * TT + tid * S;
-  const T* gin = in + gi * in_gstride;
-  if (sizeof(T) == 4 && (I & 3) == 0) {
-    for (int i4 = 0; i4 < I; i4 += 4) {
-      float4 x[S];
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        const int s = s0 + j;
-        x[j] = s < B ? __ldg(reinterpret_cast<const float4*>(gin + (int64_t)s * I + i4))
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      PackT p0, p1, p2, p3;
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        p0.v[j] = (T)x[j].x; p1.v[j] = (T)x[j].y; p2.v[j] = (T)x[j].z; p3.v[j] = (T)x[j].w;
-      }
-      *reinterpret_cast<PackT*>(vals + (int64_t)(i4 + 0) * TT + tid * S) = p0;
-      *reinterpret_cast<PackT*>(vals + (int64_t)(i4 + 1) * TT + tid * S) = p1;
-      *reinterpret_cast<PackT*>(vals + (int64_t)(i4 + 2) * TT + tid * S) = p2;
-      *reinterpret_cast<PackT*>(vals + (int64_t)(i4 + 3) * TT + tid * S) = p3;
-    }
-  } else {
-    for (int i = 0; i < I; ++i) {
-      PackT p;
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        const int s = s0 + j;
-        p.v[j] = s < B ? gin[(int64_t)s * I + i] : T(0);
-      }
-      *reinterpret_cast<PackT*>(vals + (int64_t)i * TT + tid * S) = p;
-    }
-  }
-  __syncthreads();
-
-  // node sweep in program (topological) order
-  const char* vb = reinterpret_cast<const char*>(vals) + tid * S * sizeof(T);
-  for (int k = 0; k < n_steps; ++k) {
-    const StepT<T> st = st_s[k];
-    const EdgeT<T>* ep = ed_s + st.e_begin;
-    const int ne = st.e_count;
-    const int agg = st.agg;
-    T acc[S];
-    if (agg == AGG_SUM || agg == AGG_MEAN) {
-      T a0[S], a1[S];
-#pragma unroll
-      for (int j = 0; j < S; ++j) { a0[j] = T(0); a1[j] = T(0); }
-      int e = 0;
-      for (; e + 2 <= ne; e += 2) {
-        const EdgeT<T> x0 = ep[e], x1 = ep[e + 1];
-        const PackT v0 = *reinterpret_cast<const PackT*>(vb + x0.src);
-        const PackT v1 = *reinterpret_cast<const PackT*>(vb + x1.src);
-#pragma unroll
-        for (int j = 0; j < S; ++j) {
-          a0[j] = fma(x0.w, v0.v[j], a0[j]);
-          a1[j] = fma(x1.w, v1.v[j], a1[j]);
-        }
-      }
-      if (e < ne) {
-        const EdgeT<T> x0 = ep[e];
-        const PackT v0 = *reinterpret_cast<const PackT*>(vb + x0.src);
-#pragma unroll
-        for (int j = 0; j < S; ++j) a0[j] = fma(x0.w, v0.v[j], a0[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < S; ++j) acc[j] = a0[j] + a1[j];
-    } else {
-      const T neutral = agg_neutral<T>(agg);
-#pragma unroll
-      for (int j = 0; j < S; ++j) acc[j] = neutral;
-      for (int e = 0; e < ne; ++e) {
-        const EdgeT<T> x0 = ep[e];
-        const PackT v0 = *reinterpret_cast<const PackT*>(vb + x0.src);
-#pragma unroll
-        for (int j = 0; j < S; ++j) acc[j] = agg_combine<T>(agg, acc[j], x0.w * v0.v[j]);
-      }
-    }
-    PackT y;
-#pragma unroll
-    for (int j = 0; j < S; ++j)
-      y.v[j] = apply_act(st.act, fma(st.resp, agg_finish<T>(agg, acc[j], ne), st.bias));
-    if (st.slot != NO_SLOT)
-      *reinterpret_cast<PackT*>(vals + (int64_t)st.slot * TT + tid * S) = y;
-  }
-
-  // outputs (P, B, O)
-  const uint16_t* os = reinterpret_cast<const uint16_t*>(gp + L.off_out);
-  T* go = out + gi * out_gstride;
+// finish one step: aggregate -> bias + response * agg -> activation -> slot
+template <int S, int RB>
+__device__ __forceinline__ void finish_step(const StepT<float>& st, const float (&acc)[S], char* vb) {
+  Pack<float, S> y;
+  const int act = st.act;
+  const float kx = act == ACT_TANH ? -2.8853900817779268f : (act == ACT_SIGMOID ? -1.4426950408889634f : 0.0f);
+  const float ca = act == ACT_TANH ? 2.0f : 1.0f;
+  const float cb = act == ACT_TANH ? -1.0f : 0.0f;
 #pragma unroll
   for (int j = 0; j < S; ++j) {
-    const int s = s0 + j;
-    if (s >= B) break;
-    T* row = go + (int64_t)s * O;
-    for (int o = 0; o < O; ++o) {
-      const uint16_t sl = __ldg(os + o);
-      row[o] = sl != NO_SLOT ? vals[(int64_t)sl * TT + tid * S + j] : T(NAN);
+    float a = acc[j];
+    if (st.agg == AGG_MEAN) a = st.count ? __fdividef(a, (float)st.count) : 0.0f;
+    y.v[j] = step_act(kx, ca, cb, act == ACT_RELU, fmaf(st.resp, a, st.bias));
+  }
+  if (st.slot != NO_SLOT) *reinterpret_cast<Pack<float, S>*>(vb + st.slot * RB) = y;
+}
+template <int S, int RB>
+__device__ __forceinline__ void finish_step(const StepT<double>& st, const double (&acc)[S], char* vb) {
+  Pack<double, S> y;
+#pragma unroll
+  for (int j = 0; j < S; ++j)
+    y.v[j] = apply_act(st.act, fma(st.resp, agg_finish<double>(st.agg, acc[j], st.count), st.bias));
+  if (st.slot != NO_SLOT) *reinterpret_cast<Pack<double, S>*>(vb + st.slot * RB) = y;
+}
+
+template <int N> struct U16Vec;
+template <> struct U16Vec<2> { using type = uint32_t; };
+template <> struct U16Vec<4> { using type = uint2; };
+template <> struct U16Vec<8> { using type = uint4; };
+template <int N> struct F32Vec;
+template <> struct F32Vec<2> { using type = float2; };
+template <> struct F32Vec<4> { using type = float4; };
+
+template <int N>
+__device__ __forceinline__ void load_u16(const uint16_t* p, uint32_t (&out)[N]) {
+  using V = typename U16Vec<N>::type;
+  const V v = *reinterpret_cast<const V*>(p);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) { out[2 * i] = w[i] & 0xFFFFu; out[2 * i + 1] = w[i] >> 16; }
+}
+template <int N>
+__device__ __forceinline__ void load_f32(const float* p, float (&out)[N]) {
+  if constexpr (N == 2) {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    out[0] = v.x; out[1] = v.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < N / 4; ++i) {
+      const float4 v = reinterpret_cast<const float4*>(p)[i];
+      out[4 * i] = v.x; out[4 * i + 1] = v.y; out[4 * i + 2] = v.z; out[4 * i + 3] = v.w;
+    }
+  }
+}
+
+// One sum/mean group of G steps (fp32 program): edge block of width GW = G|4,
+// two rounds per iteration (2*GW sources in one <=16-byte load, weights in
+// <=2 16-byte loads) and up to 2G independent value loads / FMA chains.
+// Rounds below the shortest list run unpredicated; the tail skips holes with
+// warp-uniform predicates.  TANH: every step is tanh/sum (short epilogue).
+template <int S, int G, int RB, bool TANH>
+__device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint16_t* __restrict__ src_s,
+                                              const float* __restrict__ w_s,
+                                              const StepT<float>* __restrict__ st, char* vb) {
+  constexpr int GW = G == 3 ? 4 : G;
+  using PackT = Pack<float, S>;
+  float acc[G][S];
+#pragma unroll
+  for (int j = 0; j < G; ++j)
+#pragma unroll
+    for (int s = 0; s < S; ++s) acc[j][s] = 0.0f;
+  const uint16_t* sp = src_s + gr.e_begin;
+  const float* wp = w_s + gr.e_begin;
+  const int rounds = gr.rounds;
+  const int full = gr.cnt[G - 1] & ~1;  // every step has an edge in rounds < full
+  int r = 0;
+#pragma unroll 1
+  for (; r < full; r += 2) {
+    uint32_t sl[2 * GW];
+    float w[2 * GW];
+    load_u16<2 * GW>(sp + r * GW, sl);
+    load_f32<2 * GW>(wp + r * GW, w);
+    PackT v[2 * GW];
+#pragma unroll
+    for (int q = 0; q < 2 * GW; ++q)
+      if (q % GW < G) v[q] = *reinterpret_cast<const PackT*>(vb + sl[q] * RB);
+#pragma unroll
+    for (int q = 0; q < 2 * GW; ++q)
+      if (q % GW < G) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[q % GW][s] = fmaf(w[q], v[q].v[s], acc[q % GW][s]);
+      }
+  }
+  if (r < rounds) {
+    int cnt[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) cnt[j] = gr.cnt[j];
+    for (; r < rounds; ++r) {
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        if (r < cnt[j]) {
+          const PackT v = *reinterpret_cast<const PackT*>(vb + (uint32_t)sp[r * GW + j] * RB);
+          const float w = wp[r * GW + j];
+#pragma unroll
+          for (int s = 0; s < S; ++s) acc[j][s] = fmaf(w, v.v[s], acc[j][s]);
+        }
+      }
+    }
+  }
+  if constexpr (TANH) {
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const StepT<float> sj = st[j];
+      PackT y;
+#pragma unroll
+      for (int s = 0; s < S; ++s) y.v[s] = tanh_fast(fmaf(sj.resp, acc[j][s], sj.bias));
+      if (sj.slot != NO_SLOT) *reinterpret_cast<PackT*>(vb + sj.slot * RB) = y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < G; ++j) finish_step<S, RB>(st[j], acc[j], vb);
+  }
+}
+
+// fp64 program group (parity mode): same structure, (src, w) pairs
+template <int S, int G, int RB>
+__device__ __forceinline__ void run_sum_group_f64(const GroupRec& gr, const EdgeD* __restrict__ ed_s,
+                                                  const StepT<double>* __restrict__ st, char* vb) {
+  constexpr int GW = G == 3 ? 4 : G;
+  double acc[G][S];
+#pragma unroll
+  for (int j = 0; j < G; ++j)
+#pragma unroll
+    for (int s = 0; s < S; ++s) acc[j][s] = 0.0;
+  const EdgeD* ep = ed_s + gr.e_begin;
+  for (int r = 0; r < gr.rounds; ++r) {
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      if (r < gr.cnt[j]) {
+        const EdgeD d = ep[r * GW + j];
+        const Pack<double, S> v = *reinterpret_cast<const Pack<double, S>*>(vb + d.src * RB);
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[j][s] = fma(d.w, v.v[s], acc[j][s]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < G; ++j) finish_step<S, RB>(st[j], acc[j], vb);
+}
+
+// singleton group with a non-sum aggregation (product / max / min), exact count
+template <typename T, int S, int RB>
+__device__ __forceinline__ void run_generic_step(const GroupRec& gr, const uint16_t* __restrict__ src_s,
+                                                 const float* __restrict__ w_s, const EdgeD* __restrict__ ed_s,
+                                                 const StepT<T>& st, char* vb) {
+  T acc[S];
+  const T neutral = agg_neutral<T>(st.agg);
+#pragma unroll
+  for (int s = 0; s < S; ++s) acc[s] = neutral;
+  for (int e = 0; e < st.count; ++e) {
+    uint32_t src;
+    T w;
+    if constexpr (sizeof(T) == 8) { src = ed_s[gr.e_begin + e].src; w = ed_s[gr.e_begin + e].w; }
+    else { src = src_s[gr.e_begin + e]; w = w_s[gr.e_begin + e]; }
+    const Pack<T, S> v = *reinterpret_cast<const Pack<T, S>*>(vb + src * RB);
+#pragma unroll
+    for (int s = 0; s < S; ++s) acc[s] = agg_combine<T>(st.agg, acc[s], w * v.v[s]);
+  }
+  if (st.count == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) acc[s] = T(0);
+  }
+  StepT<T> sum_like = st;
+  sum_like.agg = AGG_SUM;  // acc already aggregated
+  finish_step<S, RB>(sum_like, acc, vb);
+}
+
+template <typename T, int S, int RB>
+__device__ __forceinline__ void run_group(const GroupRec& gr, const uint16_t* src_s, const float* w_s,
+                                          const EdgeD* ed_s, const StepT<T>* st, char* vb) {
+  if (!(gr.cls & GRP_GENERIC)) {
+    if constexpr (sizeof(T) == 4) {
+      if (gr.cls & GRP_TANH_SUM) {
+        switch (gr.n) {
+          case 1: run_sum_group<S, 1, RB, true>(gr, src_s, w_s, st, vb); break;
+          case 2: run_sum_group<S, 2, RB, true>(gr, src_s, w_s, st, vb); break;
+          case 3: run_sum_group<S, 3, RB, true>(gr, src_s, w_s, st, vb); break;
+          default: run_sum_group<S, 4, RB, true>(gr, src_s, w_s, st, vb); break;
+        }
+      } else {
+        switch (gr.n) {
+          case 1: run_sum_group<S, 1, RB, false>(gr, src_s, w_s, st, vb); break;
+          case 2: run_sum_group<S, 2, RB, false>(gr, src_s, w_s, st, vb); break;
+          case 3: run_sum_group<S, 3, RB, false>(gr, src_s, w_s, st, vb); break;
+          default: run_sum_group<S, 4, RB, false>(gr, src_s, w_s, st, vb); break;
+        }
+      }
+    } else {
+      switch (gr.n) {
+        case 1: run_sum_group_f64<S, 1, RB>(gr, ed_s, st, vb); break;
+        case 2: run_sum_group_f64<S, 2, RB>(gr, ed_s, st, vb); break;
+        case 3: run_sum_group_f64<S, 3, RB>(gr, ed_s, st, vb); break;
+        default: run_sum_group_f64<S, 4, RB>(gr, ed_s, st, vb); break;
+      }
+    }
+  } else {
+    run_generic_step<T, S, RB>(gr, src_s, w_s, ed_s, st[0], vb);
+  }
+}
+
+// grid: one CTA per (genome, run of `tpc` consecutive tiles); the genome's
+// program is staged in shared memory once and reused for every tile
+template <typename T, int S, int NT>
+__global__ void __launch_bounds__(NT, 1) fwd_tile_kernel(const uint8_t* __restrict__ prog, ProgLayout L,
+                                                      const int32_t* __restrict__ genome_ids,
+                                                      const T* __restrict__ in, int64_t in_gstride,
+                                                      int B, int I, int O, int runs, int tpc,
+                                                      T* __restrict__ out, int64_t out_gstride) {
+  constexpr int TT = NT * S;
+  constexpr int RB = (TT + S) * sizeof(T);  // bytes of one value slot row (padded by S)
+  using PackT = Pack<T, S>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int64_t task = blockIdx.x / runs;
+  const int run = (int)(blockIdx.x - task * runs);
+  const int64_t gi = genome_ids ? (int64_t)__ldg(genome_ids + task) : task;
+  const uint8_t* gp = prog + gi * L.stride;
+  const ProgHeader hdr = *reinterpret_cast<const ProgHeader*>(gp);
+  const int n_steps = hdr.n_steps, n_edges = hdr.n_edges, n_groups = hdr.n_groups;
+  const int tid = threadIdx.x;
+
+  // shared memory: groups | steps | edge sources | edge weights | values [slot][TT]
+  GroupRec* gr_s = reinterpret_cast<GroupRec*>(smem);
+  const int64_t off_st = (int64_t)n_groups * sizeof(GroupRec);
+  StepT<T>* st_s = reinterpret_cast<StepT<T>*>(smem + off_st);
+  const int64_t off_src = off_st + (int64_t)n_steps * sizeof(StepT<T>);
+  const int64_t src_bytes = sizeof(T) == 8 ? 0 : align_up(2ll * n_edges, 16);
+  const int64_t off_w = off_src + src_bytes;
+  const int64_t w_bytes = sizeof(T) == 8 ? 16ll * n_edges : 4ll * n_edges;
+  uint16_t* src_s = reinterpret_cast<uint16_t*>(smem + off_src);
+  float* w_s = reinterpret_cast<float*>(smem + off_w);
+  EdgeD* ed_s = reinterpret_cast<EdgeD*>(smem + off_w);
+  T* vals = reinterpret_cast<T*>(smem + align_up(off_w + w_bytes, 16));
+  {
+    auto copy16 = [&](void* dst, const void* src, int64_t bytes) {
+      const int n16 = (int)(bytes / 16);
+      for (int i = tid; i < n16; i += NT)
+        reinterpret_cast<int4*>(dst)[i] = __ldg(reinterpret_cast<const int4*>(src) + i);
+    };
+    copy16(gr_s, gp + L.off_groups, off_st);
+    copy16(st_s, gp + L.off_steps, (int64_t)n_steps * sizeof(StepT<T>));
+    if (sizeof(T) == 4) copy16(src_s, gp + L.off_src, src_bytes);
+    copy16(reinterpret_cast<void*>(smem + off_w), gp + L.off_w, w_bytes);
+  }
+  // output slots of this genome (first 8 staged in shared memory)
+  const uint16_t* os = reinterpret_cast<const uint16_t*>(gp + L.off_out);
+  __shared__ uint16_t oslot[8];
+  if (tid < 8) oslot[tid] = tid < O ? __ldg(os + tid) : NO_SLOT;
+  __syncthreads();
+
+  const T* gin = in + gi * in_gstride;
+  T* go = out + gi * out_gstride;
+  char* vb = reinterpret_cast<char*>(vals) + tid * S * sizeof(T);
+  const int tile_end = min((run + 1) * tpc, (B + TT - 1) / TT);
+  const bool vec_in = sizeof(T) == 4 && (I & 3) == 0 && (in_gstride & 3) == 0;
+  const int step_s = (4 * NT) / I, step_i = (4 * NT) - step_s * I;  // chunk stride in (sample, input)
+  const int step_s1 = NT / I, step_i1 = NT - step_s1 * I;
+  // inputs -> value slots 0..I-1 (input key i lives in slot i).  A tile's
+  // (samples x I) block is contiguous in HBM: it is read with coalesced 16-byte
+  // loads and scattered into the [slot][sample] layout (rows padded by S
+  // elements, so a warp's scattered stores hit distinct banks).  The next
+  // tile's chunks are prefetched into registers while this tile computes, so
+  // the HBM latency is off the critical path.
+  constexpr int PFMAX = 4 * S;
+  const bool prefetch = vec_in && S * I / 4 <= PFMAX;
+  const int per_thread = S * I / 4;
+  float4 pf[PFMAX];
+#define TNEAT_ISSUE(tile_)                                                                \
+  {                                                                                       \
+    const int t0_ = (tile_) * TT, n4_ = min(TT, B - t0_) * I / 4;                         \
+    const float4* src_ = reinterpret_cast<const float4*>(gin + (int64_t)t0_ * I);         \
+    _Pragma("unroll") for (int k = 0; k < PFMAX; ++k) {                                   \
+      const int c = tid + k * NT;                                                         \
+      if (k < per_thread && c < n4_) pf[k] = __ldg(src_ + c);                             \
+    }                                                                                     \
+  }
+  float* const vf = reinterpret_cast<float*>(vals);
+#define TNEAT_SCATTER4(sm_, i_, x_)                 \
+  {                                                 \
+    float* base_ = vf + (sm_) + (i_) * (RB / 4);    \
+    base_[0] = (x_).x;                              \
+    base_[RB / 4] = (x_).y;                         \
+    base_[2 * (RB / 4)] = (x_).z;                   \
+    base_[3 * (RB / 4)] = (x_).w;                   \
+  }
+  if (prefetch) TNEAT_ISSUE(run * tpc);
+  for (int tile = run * tpc; tile < tile_end; ++tile) {
+    const int t0 = tile * TT;
+    const int nt = min(TT, B - t0);
+    if (tile != run * tpc) __syncthreads();  // previous tile fully consumed
+    if (prefetch) {
+      const int n4 = nt * I / 4;
+      int sm = (4 * tid) / I, i = 4 * tid - sm * I;
+#pragma unroll
+      for (int k = 0; k < PFMAX; ++k) {
+        const int c = tid + k * NT;
+        if (k < per_thread && c < n4) TNEAT_SCATTER4(sm, i, pf[k]);
+        i += step_i;
+        sm += step_s;
+        if (i >= I) { i -= I; ++sm; }
+      }
+      if (tile + 1 < tile_end) TNEAT_ISSUE(tile + 1);
+    } else if (vec_in) {
+      const float4* src = reinterpret_cast<const float4*>(gin + (int64_t)t0 * I);
+      const int n4 = nt * I / 4;
+      int sm = (4 * tid) / I, i = 4 * tid - sm * I;  // (sample, input) of chunk c, stepped
+      for (int c = tid; c < n4; c += NT) {           // incrementally (no division)
+        const float4 x = __ldg(src + c);
+        TNEAT_SCATTER4(sm, i, x);
+        i += step_i;
+        sm += step_s;
+        if (i >= I) { i -= I; ++sm; }
+      }
+    } else {
+      const T* src = gin + (int64_t)t0 * I;
+      int sm = tid / I, i = tid - sm * I;
+      for (int c = tid; c < nt * I; c += NT) {
+        reinterpret_cast<T*>(reinterpret_cast<char*>(vals) + i * RB)[sm] = src[c];
+        i += step_i1;
+        sm += step_s1;
+        if (i >= I) { i -= I; ++sm; }
+      }
+    }
+    __syncthreads();
+    const int s0 = t0 + tid * S;
+
+    // node sweep, one group of independent same-level nodes at a time
+#pragma unroll 1
+    for (int g = 0; g < n_groups; ++g) {
+      const GroupRec gr = gr_s[g];
+      run_group<T, S, RB>(gr, src_s, w_s, ed_s, st_s + gr.step_begin, vb);
+    }
+
+    // outputs (P, B, O)
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const int s = s0 + j;
+      if (s >= B) break;
+      T y[8];
+#pragma unroll
+      for (int o = 0; o < 8; ++o)
+        y[o] = o < O ? (oslot[o] != NO_SLOT ? *reinterpret_cast<const T*>(vb + oslot[o] * RB + j * sizeof(T)) : T(NAN)) : T(0);
+      T* row = go + (int64_t)s * O;
+      if (sizeof(T) == 4 && O == 8) {
+        reinterpret_cast<float4*>(row)[0] = make_float4(y[0], y[1], y[2], y[3]);
+        reinterpret_cast<float4*>(row)[1] = make_float4(y[4], y[5], y[6], y[7]);
+      } else if (O <= 8) {
+#pragma unroll
+        for (int o = 0; o < 8; ++o)
+          if (o < O) row[o] = y[o];
+      } else {
+        for (int o = 0; o < O; ++o) {
+          const uint16_t sl = __ldg(os + o);
+          row[o] = sl != NO_SLOT ? *reinterpret_cast<const T*>(vb + sl * RB + j * sizeof(T)) : T(NAN);
+        }
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// warp-per-genome kernel for small batches
+// warp-per-(genome, input chunk) kernel for small batches
 // ---------------------------------------------------------------------------
 
 template <typename T> __device__ __forceinline__ T warp_allreduce(int agg, T v) {
@@ -170,90 +408,153 @@ template <typename T> __device__ __forceinline__ T warp_allreduce(int agg, T v) 
   return v;
 }
 
+template <typename T> __device__ __forceinline__ T eval_node(const StepT<T>& st, T a);
+template <> __device__ __forceinline__ float eval_node<float>(const StepT<float>& st, float a) {
+  a = agg_finish<float>(st.agg, a, st.count);
+  const int act = st.act;
+  const float kx = act == ACT_TANH ? -2.8853900817779268f : (act == ACT_SIGMOID ? -1.4426950408889634f : 0.0f);
+  return step_act(kx, act == ACT_TANH ? 2.0f : 1.0f, act == ACT_TANH ? -1.0f : 0.0f, act == ACT_RELU,
+                  fmaf(st.resp, a, st.bias));
+}
+template <> __device__ __forceinline__ double eval_node<double>(const StepT<double>& st, double a) {
+  return apply_act(st.act, fma(st.resp, agg_finish<double>(st.agg, a, st.count), st.bias));
+}
+
 enum : int { FIT_NONE = 0, FIT_XOR = 1, FIT_REGRESSION = 2 };
 
 template <typename T>
 __global__ void fwd_warp_kernel(const uint8_t* __restrict__ prog, ProgLayout L, int64_t P,
                                 const T* __restrict__ in, int64_t in_gstride, int B, int I, int O,
-                                int max_slots, T* __restrict__ out, int64_t out_gstride,
+                                int bchunk, int max_slots, T* __restrict__ out, int64_t out_gstride,
                                 int fit_kind, const double* __restrict__ targets,
                                 double* __restrict__ fitness) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t gi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  const int chunks = (B + bchunk - 1) / bchunk;
+  const int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  const int64_t gi = task / chunks;
   if (gi >= P) return;
-  T* vals = reinterpret_cast<T*>(smem) + (int64_t)warp * max_slots * B;  // [slot][B]
+  const int b0 = (int)(task - gi * chunks) * bchunk;
+  const int nb = min(bchunk, B - b0);
+  T* vals = reinterpret_cast<T*>(smem) + (int64_t)warp * max_slots * bchunk;  // [slot][bchunk]
   const uint8_t* gp = prog + gi * L.stride;
   const ProgHeader hdr = *reinterpret_cast<const ProgHeader*>(gp);
+  const GroupRec* groups = reinterpret_cast<const GroupRec*>(gp + L.off_groups);
   const StepT<T>* steps = reinterpret_cast<const StepT<T>*>(gp + L.off_steps);
-  const EdgeT<T>* edges = reinterpret_cast<const EdgeT<T>*>(gp + L.off_edges);
-  const T* gin = in + gi * in_gstride;
-  for (int idx = lane; idx < B * I; idx += 32) {
+  const uint16_t* esrc = reinterpret_cast<const uint16_t*>(gp + L.off_src);
+  const float* ew = reinterpret_cast<const float*>(gp + L.off_w);
+  const EdgeD* ed = reinterpret_cast<const EdgeD*>(gp + L.off_w);
+  const T* gin = in + gi * in_gstride + (int64_t)b0 * I;
+  for (int idx = lane; idx < nb * I; idx += 32) {
     const int b = idx / I, i = idx - b * I;
-    vals[i * B + b] = gin[idx];
+    vals[i * bchunk + b] = gin[idx];
   }
   __syncwarp();
-  for (int k = 0; k < hdr.n_steps; ++k) {
-    const StepT<T> st = steps[k];
-    const int agg = st.agg, ne = st.e_count;
-    for (int b = 0; b < B; ++b) {
-      T part = agg_neutral<T>(agg);
-      for (int e = lane; e < ne; e += 32) {
-        const EdgeT<T> x = edges[st.e_begin + e];
-        part = agg_combine<T>(agg, part, x.w * vals[(int64_t)x.src * B + b]);
+  for (int g = 0; g < hdr.n_groups; ++g) {
+    const GroupRec gr = groups[g];
+    const int gw = group_width(gr.n);
+    for (int b = 0; b < nb; ++b) {
+      T y[4];
+      for (int j = 0; j < gr.n; ++j) {  // all reads of the group precede its writes
+        const StepT<T> st = steps[gr.step_begin + j];
+        const int agg = st.agg;
+        const int stride = (gr.cls & GRP_GENERIC) ? 1 : gw;
+        T part = agg_neutral<T>(agg);
+        for (int e = lane; e < st.count; e += 32) {
+          const int idx = gr.e_begin + e * stride + j;
+          uint32_t src;
+          T w;
+          if constexpr (sizeof(T) == 8) { src = ed[idx].src; w = ed[idx].w; }
+          else { src = esrc[idx]; w = ew[idx]; }
+          part = agg_combine<T>(agg, part, w * vals[(int64_t)src * bchunk + b]);
+        }
+        y[j & 3] = eval_node<T>(st, warp_allreduce<T>(agg, part));
       }
-      const T a = warp_allreduce<T>(agg, part);
-      if (lane == 0 && st.slot != NO_SLOT)
-        vals[(int64_t)st.slot * B + b] = apply_act(st.act, fma(st.resp, agg_finish<T>(agg, a, ne), st.bias));
+      __syncwarp();
+      if (lane == 0) {
+        for (int j = 0; j < gr.n; ++j) {
+          const uint16_t sl = steps[gr.step_begin + j].slot;
+          if (sl != NO_SLOT) vals[(int64_t)sl * bchunk + b] = y[j & 3];
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
   const uint16_t* os = reinterpret_cast<const uint16_t*>(gp + L.off_out);
   if (fit_kind == FIT_NONE) {
-    T* go = out + gi * out_gstride;
-    for (int idx = lane; idx < B * O; idx += 32) {
+    T* go = out + gi * out_gstride + (int64_t)b0 * O;
+    for (int idx = lane; idx < nb * O; idx += 32) {
       const int b = idx / O, o = idx - b * O;
       const uint16_t sl = os[o];
-      go[idx] = sl != NO_SLOT ? vals[(int64_t)sl * B + b] : T(NAN);
+      go[idx] = sl != NO_SLOT ? vals[(int64_t)sl * bchunk + b] : T(NAN);
     }
   } else if (lane == 0) {
-    // fitness in float64 (problems.py:54-61), summation order of numpy for n < 8
-    // (sequential) and 8-way pairwise blocks for 8 <= n <= 128
+    // fitness in float64 (problems.py:54-61) with numpy's summation order:
+    // sequential below 8 terms, else 8 strided partial sums combined pairwise,
+    // then the remainder added one by one
     const uint16_t sl = os[0];
-    double r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    double acc = 0.0;
-    const bool blocked = B >= 8;
-    for (int b = 0; b < B; ++b) {
-      const double y = (double)vals[(int64_t)sl * B + b];
+    auto term = [&](int b) {
+      const double y = (double)vals[(int64_t)sl * bchunk + b];
       const double t = fit_kind == FIT_XOR ? (double)(((b >> 1) ^ b) & 1) : targets[b];
-      const double d = (y - t) * (y - t);
-      if (blocked) {
-        if (b < (B & ~7)) r[b & 7] += d; else acc += d;
-      } else {
-        acc += d;
-      }
+      return (y - t) * (y - t);
+    };
+    double total = 0.0;
+    int b = 0;
+    if (B >= 8) {
+      double r[8];
+      for (int j = 0; j < 8; ++j) r[j] = term(j);
+      for (b = 8; b + 8 <= B; b += 8)
+        for (int j = 0; j < 8; ++j) r[j] += term(b + j);
+      total = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
     }
-    double total = acc;
-    if (blocked) total = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7])) + acc;
+    for (; b < B; ++b) total += term(b);
     fitness[gi] = fit_kind == FIT_XOR ? 4.0 - total : -(total / (double)B);
   }
 }
 
-template <typename T, int S, int NT>
-int launch_tile(const uint8_t* prog, const ProgLayout& L, const T* in, int64_t in_gstride, int64_t P,
+template <typename T>
+int launch_warp(const uint8_t* prog, const ProgLayout& L, int64_t P, const T* in, int64_t in_gstride,
                 int B, int I, int O, const int32_t* maxdims_host, T* out, int64_t out_gstride,
-                cudaStream_t st) {
+                int fit_kind, const double* targets, double* fitness, cudaStream_t st) {
+  const int slots = maxdims_host[0] > 0 ? maxdims_host[0] : I + 1;
+  int bchunk = B;
+  if (fit_kind == FIT_NONE) {
+    const int cap = (int)((48 * 1024) / ((int64_t)slots * sizeof(T)));
+    bchunk = max(1, min(B, cap));
+  }
+  const int64_t per_warp = (int64_t)slots * bchunk * sizeof(T);
+  int wpb = 4;
+  while (wpb > 1 && per_warp * wpb > 200 * 1024) wpb >>= 1;
+  if (per_warp * wpb > 227 * 1024) return -6;
+  const int64_t tasks = P * ((B + bchunk - 1) / bchunk);
+  const int64_t blocks = (tasks + wpb - 1) / wpb;
+  const int64_t smem = per_warp * wpb;
+  cudaFuncSetAttribute(fwd_warp_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  fwd_warp_kernel<T><<<(unsigned)blocks, 32 * wpb, smem, st>>>(prog, L, P, in, in_gstride, B, I, O, bchunk,
+                                                               slots, out, out_gstride, fit_kind, targets,
+                                                               fitness);
+  TNEAT_CHECK_LAUNCH();
+  return 0;
+}
+
+template <typename T, int S, int NT>
+int launch_tile(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, const T* in, int64_t in_gstride,
+                int64_t P, int B, int I, int O, const int32_t* maxdims_host, T* out, int64_t out_gstride,
+                int tpc, cudaStream_t st) {
   constexpr int TT = NT * S;
   const int tiles = (B + TT - 1) / TT;
-  const int64_t grid = P * tiles;
+  tpc = max(1, min(tpc, tiles));
+  const int runs = (tiles + tpc - 1) / tpc;
+  const int64_t grid = P * runs;
   if (grid > 0x7FFFFFFFll) return -5;
-  const int64_t smem = align_up((int64_t)maxdims_host[1] * sizeof(StepT<T>), 16) +
-                       align_up((int64_t)maxdims_host[2] * sizeof(EdgeT<T>), 16) +
-                       (int64_t)maxdims_host[0] * TT * sizeof(T);
+  const int64_t ms = maxdims_host[1], me = maxdims_host[2];
+  const int64_t prog_bytes = ms * sizeof(GroupRec) + ms * sizeof(StepT<T>) +
+                             (sizeof(T) == 8 ? 16 * me : align_up(2 * me, 16) + 4 * me);
+  const int64_t smem = align_up(prog_bytes, 16) + (int64_t)max(maxdims_host[0], I) * (TT + S) * sizeof(T);
   if (smem > 227 * 1024) return -6;
   cudaFuncSetAttribute(fwd_tile_kernel<T, S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fwd_tile_kernel<T, S, NT><<<(unsigned)grid, NT, smem, st>>>(prog, L, in, in_gstride, B, I, O, tiles,
+  fwd_tile_kernel<T, S, NT><<<(unsigned)grid, NT, smem, st>>>(prog, L, ids, in, in_gstride, B, I, O, runs, tpc,
                                                               out, out_gstride);
   TNEAT_CHECK_LAUNCH();
   return 0;
@@ -267,8 +568,9 @@ extern "C" {
 
 // Replaces inference.forward_arrays (inference.py:185-262).  See include/tneat.h.
 int an_forward(const void* program, int64_t program_stride, int N, int C, int precision,
-               const int32_t* maxdims_host, const void* inputs, int64_t input_genome_stride,
-               int64_t P, int B, int I, int O, void* outputs, int variant, void* stream) {
+               const int32_t* maxdims_host, const int32_t* genome_ids, const void* inputs,
+               int64_t input_genome_stride, int64_t P, int B, int I, int O, void* outputs, int variant,
+               void* stream) {
   if (P < 0 || B < 0 || I < 1 || O < 1 || !maxdims_host) return -1;
   if (P == 0 || B == 0) return 0;
   if (!program || !inputs || !outputs) return -2;
@@ -277,39 +579,38 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
   cudaStream_t st = (cudaStream_t)stream;
   const uint8_t* pg = (const uint8_t*)program;
   const int64_t ogs = (int64_t)B * O;
-  // variant: 0 = auto, 1 = tile S=1, 2 = tile S=2, 4 = tile S=4, 8 = warp kernel
-  if (variant == 0) variant = B >= 96 ? 2 : 8;
+  // variant (low 4 bits): 0 = auto, 1 = tile S=1 (128 thr), 2 = tile S=2 (128 thr),
+  // 3 = tile S=1 (64 thr), 4 = tile S=4 (64 thr), 5 = tile S=2 (64 thr), 6 = tile S=4 (32 thr),
+  // 8 = warp kernel; bits 8..15 = tiles per CTA (0 = default 4)
+  int tpc = (variant >> 8) & 0xFF;
+  if (tpc == 0) tpc = 4;
+  variant &= 0xF;
+  if (variant == 0) variant = B >= 192 ? 5 : (B >= 96 ? 3 : 8);
   if (variant == 8) {
-    const int wpb = 4;
-    const int64_t smem = (int64_t)wpb * maxdims_host[0] * B * (precision ? 8 : 4);
-    if (smem > 227 * 1024) return -6;
-    const int64_t blocks = (P + wpb - 1) / wpb;
-    if (precision) {
-      cudaFuncSetAttribute(fwd_warp_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      fwd_warp_kernel<double><<<(unsigned)blocks, 32 * wpb, smem, st>>>(
-          pg, L, P, (const double*)inputs, input_genome_stride, B, I, O, maxdims_host[0],
-          (double*)outputs, ogs, FIT_NONE, nullptr, nullptr);
-    } else {
-      cudaFuncSetAttribute(fwd_warp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      fwd_warp_kernel<float><<<(unsigned)blocks, 32 * wpb, smem, st>>>(
-          pg, L, P, (const float*)inputs, input_genome_stride, B, I, O, maxdims_host[0],
-          (float*)outputs, ogs, FIT_NONE, nullptr, nullptr);
-    }
-    TNEAT_CHECK_LAUNCH();
-    return 0;
+    if (genome_ids) return -7;
+    if (precision)
+      return launch_warp<double>(pg, L, P, (const double*)inputs, input_genome_stride, B, I, O, maxdims_host,
+                                 (double*)outputs, ogs, FIT_NONE, nullptr, nullptr, st);
+    return launch_warp<float>(pg, L, P, (const float*)inputs, input_genome_stride, B, I, O, maxdims_host,
+                              (float*)outputs, ogs, FIT_NONE, nullptr, nullptr, st);
   }
+  const int32_t* ids = genome_ids;
   if (precision) {
     const double* in = (const double*)inputs;
     double* out = (double*)outputs;
-    if (variant == 1) return launch_tile<double, 1, 128>(pg, L, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, st);
-    return launch_tile<double, 2, 64>(pg, L, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, st);
+    if (variant == 2 || variant == 5)
+      return launch_tile<double, 2, 64>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
+    return launch_tile<double, 1, 128>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
   }
   const float* in = (const float*)inputs;
   float* out = (float*)outputs;
   switch (variant) {
-    case 1: return launch_tile<float, 1, 128>(pg, L, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, st);
-    case 4: return launch_tile<float, 4, 64>(pg, L, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, st);
-    default: return launch_tile<float, 2, 64>(pg, L, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, st);
+    case 2: return launch_tile<float, 2, 128>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
+    case 3: return launch_tile<float, 1, 64>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
+    case 4: return launch_tile<float, 4, 64>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
+    case 5: return launch_tile<float, 2, 64>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
+    case 6: return launch_tile<float, 4, 32>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
+    default: return launch_tile<float, 1, 128>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
   }
 }
 
@@ -326,23 +627,11 @@ int an_forward_fitness(const void* program, int64_t program_stride, int N, int C
   const ProgLayout L = prog_layout(N, C, O, precision);
   if (L.stride != program_stride) return -3;
   cudaStream_t st = (cudaStream_t)stream;
-  const int wpb = 4;
-  const int64_t smem = (int64_t)wpb * maxdims_host[0] * B * (precision ? 8 : 4);
-  if (smem > 227 * 1024) return -6;
-  const int64_t blocks = (P + wpb - 1) / wpb;
-  if (precision) {
-    cudaFuncSetAttribute(fwd_warp_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    fwd_warp_kernel<double><<<(unsigned)blocks, 32 * wpb, smem, st>>>(
-        (const uint8_t*)program, L, P, (const double*)inputs, input_genome_stride, B, I, O,
-        maxdims_host[0], nullptr, 0, kind, targets, fitness);
-  } else {
-    cudaFuncSetAttribute(fwd_warp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    fwd_warp_kernel<float><<<(unsigned)blocks, 32 * wpb, smem, st>>>(
-        (const uint8_t*)program, L, P, (const float*)inputs, input_genome_stride, B, I, O,
-        maxdims_host[0], nullptr, 0, kind, targets, fitness);
-  }
-  TNEAT_CHECK_LAUNCH();
-  return 0;
+  if (precision)
+    return launch_warp<double>((const uint8_t*)program, L, P, (const double*)inputs, input_genome_stride, B, I,
+                               O, maxdims_host, nullptr, 0, kind, targets, fitness, st);
+  return launch_warp<float>((const uint8_t*)program, L, P, (const float*)inputs, input_genome_stride, B, I, O,
+                            maxdims_host, nullptr, 0, kind, targets, fitness, st);
 }
 
 }  // extern "C"

@@ -11,29 +11,39 @@
 //     successor decrements run lane-parallel;
 //   * cyclic genomes flagged (inference.py:143).
 // The dense (P,N,N) `incoming` tensor of the reference is NOT materialised;
-// the kernel emits a per-destination CSR (the non-NaN entries of each
-// incoming row, in source-row order) inside the genome's program instead.
+// the kernel compiles each genome into a program (common.cuh): level-sorted,
+// grouped steps with per-step edge lists and liveness-recycled value slots.
 
 #include "common.cuh"
 
 namespace tneat {
 
 constexpr uint64_t U64_MAX = ~0ull;
+constexpr int32_t NEVER = 0x7FFFFFFF;
+constexpr uint8_t F_LIVE = 1, F_INPUT = 2, F_OUTPUT = 4, F_FREED = 8;
 
 struct WarpSmem {
-  uint64_t* skey;    // [Npad]   (key << 16 | row), sorted
-  uint64_t* ekey;    // [Cpad]   (dst << 48 | src << 32 | conn_row), sorted
-  int32_t* indeg;    // [N]
-  int32_t* outdeg;   // [N]
-  int32_t* in_start; // [N+1]
-  int32_t* su_start; // [N+1]
-  uint16_t* succ;    // [C]
-  uint16_t* order;   // [N]
-  uint16_t* slot_of; // [N]
-  uint8_t* flags;    // [N]  bit0 live, bit1 input, bit2 output
-  uint8_t* needed;   // [N]
-  uint8_t* used;     // [N]
-  uint32_t* ready;   // [W]
+  uint64_t* skey;     // [Npad]   (key << 16 | row), sorted
+  uint64_t* ekey;     // [Cpad]   (dst << 48 | src << 32 | conn_row), sorted
+  uint64_t* ekey2;    // [C]      unsorted staging for the counting sort
+  uint64_t* gkey;     // [Npad]   step sort keys
+  int32_t* indeg;     // [N]
+  int32_t* outdeg;    // [N]
+  int32_t* in_start;  // [N+1]    CSR by destination into ekey
+  int32_t* su_start;  // [N+1]    CSR by source into succ
+  int32_t* lvl;       // [N]      topological level
+  int32_t* last_grp;  // [N]      last group that reads the node
+  uint16_t* succ;     // [C]
+  uint16_t* order;    // [N]
+  uint16_t* slot_of;  // [N]
+  uint16_t* step_row; // [N]
+  uint16_t* grp_of;   // [N]
+  GroupRec* grp;      // [N]
+  uint8_t* flags;     // [N]
+  uint8_t* needed;    // [N]
+  uint8_t* used;      // [N]
+  uint32_t* ready;    // [W]
+  uint32_t* freemask; // [WS]
 };
 
 __host__ __device__ inline int next_pow2(int x) {
@@ -42,43 +52,54 @@ __host__ __device__ inline int next_pow2(int x) {
   return p;
 }
 
-__host__ __device__ inline int64_t warp_smem_bytes(int N, int C) {
+template <bool kCarve>
+__host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, WarpSmem* s) {
   const int Npad = next_pow2(N), Cpad = next_pow2(C);
-  const int W = (N + 31) / 32;
-  int64_t b = 0;
-  b += 8ll * Npad + 8ll * Cpad;
-  b += 4ll * N * 2 + 4ll * (N + 1) * 2;
-  b = align_up(b, 8);
-  b += 2ll * C + 2ll * N * 2;
-  b = align_up(b, 4);
-  b += 3ll * N;
-  b = align_up(b, 4);
-  b += 4ll * W;
-  return align_up(b, 16);
+  const int W = (N + 31) / 32, WS = (N + 2 + 31) / 32;
+  int64_t o = 0;
+  auto take = [&](int64_t bytes, int64_t al) {
+    o = align_up(o, al);
+    const int64_t at = o;
+    o += bytes;
+    return at;
+  };
+  const int64_t a_skey = take(8ll * Npad, 8), a_ekey = take(8ll * Cpad, 8), a_gkey = take(8ll * Npad, 8);
+  const int64_t a_ekey2 = take(8ll * (C > 0 ? C : 1), 8);
+  const int64_t a_indeg = take(4ll * N, 4), a_outdeg = take(4ll * N, 4);
+  const int64_t a_in = take(4ll * (N + 1), 4), a_su = take(4ll * (N + 1), 4);
+  const int64_t a_lvl = take(4ll * N, 4), a_last = take(4ll * N, 4);
+  const int64_t a_grp = take(16ll * N, 16);
+  const int64_t a_succ = take(2ll * C, 2), a_order = take(2ll * N, 2), a_slot = take(2ll * N, 2);
+  const int64_t a_srow = take(2ll * N, 2), a_grpof = take(2ll * N, 2);
+  const int64_t a_flags = take(N, 1), a_needed = take(N, 1), a_used = take(N, 1);
+  const int64_t a_ready = take(4ll * W, 4), a_free = take(4ll * WS, 4);
+  if (kCarve) {
+    s->skey = (uint64_t*)(base + a_skey);
+    s->ekey = (uint64_t*)(base + a_ekey);
+    s->ekey2 = (uint64_t*)(base + a_ekey2);
+    s->gkey = (uint64_t*)(base + a_gkey);
+    s->indeg = (int32_t*)(base + a_indeg);
+    s->outdeg = (int32_t*)(base + a_outdeg);
+    s->in_start = (int32_t*)(base + a_in);
+    s->su_start = (int32_t*)(base + a_su);
+    s->lvl = (int32_t*)(base + a_lvl);
+    s->last_grp = (int32_t*)(base + a_last);
+    s->grp = (GroupRec*)(base + a_grp);
+    s->succ = (uint16_t*)(base + a_succ);
+    s->order = (uint16_t*)(base + a_order);
+    s->slot_of = (uint16_t*)(base + a_slot);
+    s->step_row = (uint16_t*)(base + a_srow);
+    s->grp_of = (uint16_t*)(base + a_grpof);
+    s->flags = base + a_flags;
+    s->needed = base + a_needed;
+    s->used = base + a_used;
+    s->ready = (uint32_t*)(base + a_ready);
+    s->freemask = (uint32_t*)(base + a_free);
+  }
+  return align_up(o, 16);
 }
 
-__device__ inline WarpSmem carve(uint8_t* base, int N, int C) {
-  const int Npad = next_pow2(N), Cpad = next_pow2(C);
-  WarpSmem s;
-  uint8_t* p = base;
-  s.skey = (uint64_t*)p; p += 8ll * Npad;
-  s.ekey = (uint64_t*)p; p += 8ll * Cpad;
-  s.indeg = (int32_t*)p; p += 4ll * N;
-  s.outdeg = (int32_t*)p; p += 4ll * N;
-  s.in_start = (int32_t*)p; p += 4ll * (N + 1);
-  s.su_start = (int32_t*)p; p += 4ll * (N + 1);
-  p = base + align_up(p - base, 8);
-  s.succ = (uint16_t*)p; p += 2ll * C;
-  s.order = (uint16_t*)p; p += 2ll * N;
-  s.slot_of = (uint16_t*)p; p += 2ll * N;
-  p = base + align_up(p - base, 4);
-  s.flags = p; p += N;
-  s.needed = p; p += N;
-  s.used = p; p += N;
-  p = base + align_up(p - base, 4);
-  s.ready = (uint32_t*)p;
-  return s;
-}
+__host__ inline int64_t warp_smem_bytes(int N, int C) { return layout_warp<false>(nullptr, N, C, nullptr); }
 
 // ascending bitonic sort of n (power of two, >= 32) u64 values, one warp
 __device__ void warp_bitonic_sort(uint64_t* a, int n) {
@@ -133,6 +154,17 @@ __device__ inline bool key_ok(double k) {
   return k >= 0.0 && k < 140737488355328.0 /* 2^47 */ && k == floor(k);
 }
 
+// lowest set bit over words[0..nw) (lane-strided ownership); -1 if none
+__device__ inline int warp_first_set(const uint32_t* words, int nw) {
+  const int lane = threadIdx.x & 31;
+  unsigned mine = 0xFFFFFFFFu;
+  for (int w = lane; w < nw; w += 32)
+    if (words[w]) { mine = (unsigned)w; break; }
+  const unsigned wmin = __reduce_min_sync(0xffffffffu, mine);
+  if (wmin == 0xFFFFFFFFu) return -1;
+  return (int)wmin * 32 + __ffs(words[wmin]) - 1;
+}
+
 template <typename T>
 __global__ void transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
                                  int64_t P, int N, int C, int I, int O, int mode, int prune,
@@ -145,25 +177,27 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   const int warp = threadIdx.x >> 5;
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (g >= P) return;
-  WarpSmem s = carve(smem + warp * wsmem, N, C);
+  WarpSmem s;
+  layout_warp<true>(smem + warp * wsmem, N, C, &s);
   const int Npad = next_pow2(N);
   const double* gn = nodes + g * (int64_t)N * 5;
   const double* gc = conns + g * (int64_t)C * 4;
   const int io = I + O;
+  const bool recurrent = mode == 1;
   int status = 0;
 
   // ---- nodes: live mask, key table ------------------------------------------
   int n_live = 0;
   for (int r = lane; r < Npad; r += 32) {
     uint64_t packed = U64_MAX;
-    uint8_t f = 0;
     if (r < N) {
+      uint8_t f = 0;
       const double k = gn[(int64_t)r * 5];
       if (!isnan(k)) {
         if (!key_ok(k)) status |= ST_BAD_KEY;
         const uint64_t ki = (uint64_t)k;
         packed = (ki << 16) | (uint64_t)r;
-        f = 1 | (ki < (uint64_t)I ? 2 : 0) | (ki >= (uint64_t)I && ki < (uint64_t)io ? 4 : 0);
+        f = F_LIVE | (ki < (uint64_t)I ? F_INPUT : 0) | (ki >= (uint64_t)I && ki < (uint64_t)io ? F_OUTPUT : 0);
         ++n_live;
       }
       s.flags[r] = f;
@@ -171,6 +205,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       s.used[r] = 0;
       s.indeg[r] = 0;
       s.outdeg[r] = 0;
+      s.lvl[r] = 0;
       s.slot_of[r] = NO_SLOT;
     }
     s.skey[r] = packed;
@@ -206,65 +241,67 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     const unsigned m = __ballot_sync(0xffffffffu, en);
     if (en) {
       const int pos = n_en + __popc(m & ((1u << lane) - 1));
-      s.ekey[pos] = ((uint64_t)dr << 48) | ((uint64_t)sr << 32) | (uint64_t)c;
+      s.ekey2[pos] = ((uint64_t)dr << 48) | ((uint64_t)sr << 32) | (uint64_t)c;
     }
     n_en += __popc(m);
   }
-  const int Epad = next_pow2(n_en);
-  for (int i = n_en + lane; i < Epad; i += 32) s.ekey[i] = U64_MAX;
   __syncwarp();
-  warp_bitonic_sort(s.ekey, Epad);
 
-  // ---- degrees, CSR by destination (sorted) and by source ---------------------
+  // ---- counting sort by destination, then by source inside each bucket; CSR by
+  // destination (in_start) and by source (su_start/succ) ------------------------
   for (int e = lane; e < n_en; e += 32) {
-    const uint64_t k = s.ekey[e];
+    const uint64_t k = s.ekey2[e];
     atomicAdd(&s.indeg[(int)((k >> 48) & 0xFFFF)], 1);
     atomicAdd(&s.outdeg[(int)((k >> 32) & 0xFFFF)], 1);
   }
   __syncwarp();
   warp_exclusive_scan(s.indeg, s.in_start, N);
   warp_exclusive_scan(s.outdeg, s.su_start, N);
-  // fill successor lists (order within a source is irrelevant to Kahn);
-  // outdeg doubles as the per-source cursor
-  for (int r = lane; r < N; r += 32) s.outdeg[r] = 0;
+  for (int r = lane; r < N; r += 32) { s.outdeg[r] = 0; s.lvl[r] = 0; }  // cursors
   __syncwarp();
   for (int e = lane; e < n_en; e += 32) {
-    const uint64_t k = s.ekey[e];
-    const int sr = (int)((k >> 32) & 0xFFFF);
-    const int pos = s.su_start[sr] + atomicAdd(&s.outdeg[sr], 1);
-    s.succ[pos] = (uint16_t)((k >> 48) & 0xFFFF);
+    const uint64_t k = s.ekey2[e];
+    const int dr = (int)((k >> 48) & 0xFFFF), sr = (int)((k >> 32) & 0xFFFF);
+    s.ekey[s.in_start[dr] + atomicAdd(&s.lvl[dr], 1)] = k;
+    s.succ[s.su_start[sr] + atomicAdd(&s.outdeg[sr], 1)] = (uint16_t)dr;
+  }
+  __syncwarp();
+  for (int r = lane; r < N; r += 32) {  // insertion sort of each (small) bucket
+    const int b0 = s.in_start[r], b1 = s.in_start[r + 1];
+    for (int i = b0 + 1; i < b1; ++i) {
+      const uint64_t x = s.ekey[i];
+      int j = i - 1;
+      while (j >= b0 && s.ekey[j] > x) { s.ekey[j + 1] = s.ekey[j]; --j; }
+      s.ekey[j + 1] = x;
+    }
+    s.lvl[r] = 0;
   }
   __syncwarp();
 
-  // ---- Kahn, smallest ready row first (inference.py:127-141) ------------------
+  // ---- Kahn, smallest ready row first (inference.py:127-141) + levels ---------
   const int W = (N + 31) / 32;
   for (int w = 0; w < W; ++w) {
     const int r = w * 32 + lane;
-    const bool rdy = r < N && (s.flags[r] & 1) && s.indeg[r] == 0;
+    const bool rdy = r < N && (s.flags[r] & F_LIVE) && s.indeg[r] == 0;
     const unsigned m = __ballot_sync(0xffffffffu, rdy);
     if (lane == 0) s.ready[w] = m;
   }
   __syncwarp();
   int n_order = 0;
   for (; n_order < n_live; ++n_order) {
-    unsigned mine = 0xFFFFFFFFu;
-    for (int w = lane; w < W; w += 32) {
-      if (s.ready[w]) { mine = (unsigned)w; break; }
-    }
-    const unsigned wmin = __reduce_min_sync(0xffffffffu, mine);
-    if (wmin == 0xFFFFFFFFu) break;
-    const uint32_t word = s.ready[wmin];
-    const int bit = __ffs(word) - 1;
-    const int pick = (int)wmin * 32 + bit;
+    const int pick = warp_first_set(s.ready, W);
+    if (pick < 0) break;
     __syncwarp();
     if (lane == 0) {
-      s.ready[wmin] = word & ~(1u << bit);
+      s.ready[pick >> 5] &= ~(1u << (pick & 31));
       s.order[n_order] = (uint16_t)pick;
     }
     __syncwarp();
+    const int nl = s.lvl[pick] + 1;
     const int e1 = s.su_start[pick + 1];
     for (int e = s.su_start[pick] + lane; e < e1; e += 32) {
       const int d = s.succ[e];
+      atomicMax(&s.lvl[d], nl);
       if (atomicSub(&s.indeg[d], 1) == 1) atomicOr(&s.ready[d >> 5], 1u << (d & 31));
     }
     __syncwarp();
@@ -285,7 +322,6 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
 
   uint8_t* gp = prog + g * L.stride;
   ProgHeader* hdr = (ProgHeader*)gp;
-  const bool recurrent = mode == 1;
   if ((status & ~ST_CYCLIC) || ((status & ST_CYCLIC) && !recurrent)) {
     if (lane == 0) {
       ProgHeader h{0, 0, I, n_order, status, n_live, mode, 0};
@@ -298,11 +334,11 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   // ---- which nodes matter (ancestor cone of the outputs) and which are read ----
   if (!recurrent && prune) {
     for (int r = lane; r < N; r += 32)
-      if (s.flags[r] & 4) s.needed[r] = 1;
+      if (s.flags[r] & F_OUTPUT) s.needed[r] = 1;
     __syncwarp();
     for (int i = n_order - 1; i >= 0; --i) {
       const int r = s.order[i];
-      if (!s.needed[r] || (s.flags[r] & 2)) continue;
+      if (!s.needed[r] || (s.flags[r] & F_INPUT)) continue;
       for (int e = s.in_start[r] + lane; e < s.in_start[r + 1]; e += 32) {
         const int sr = (int)((s.ekey[e] >> 32) & 0xFFFF);
         s.needed[sr] = 1;
@@ -312,92 +348,178 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     }
   } else {
     for (int r = lane; r < N; r += 32) {
-      s.needed[r] = (s.flags[r] & 1) ? 1 : 0;
-      s.used[r] = (s.su_start[r + 1] > s.su_start[r]) ? 1 : 0;
+      s.needed[r] = (s.flags[r] & F_LIVE) ? 1 : 0;
+      s.used[r] = (recurrent || s.su_start[r + 1] > s.su_start[r]) ? 1 : 0;
     }
   }
   __syncwarp();
 
-  // ---- steps: the order (ff) or every live non-input row (recurrent) ----------
-  // feed-forward steps keep a slot only when read later or an output; recurrent
-  // steps all keep one (their value is the next step's state)
-  int n_steps = 0, n_edges = 0, n_store = 0;
+  // ---- steps: emitted nodes sorted by (level, class, -count, position) --------
+  // feed-forward: positions in the Kahn order; recurrent: rows (all nodes are
+  // state, singleton groups, no slot recycling)
   const int n_pos = recurrent ? N : n_order;
-  StepT<T>* steps = (StepT<T>*)(gp + L.off_steps);
-  EdgeT<T>* edges = (EdgeT<T>*)(gp + L.off_edges);
-  for (int r = lane; r < N; r += 32)
-    if (s.flags[r] & 2) s.slot_of[r] = (uint16_t)(gn[(int64_t)r * 5] );  // input key i -> slot i
-  __syncwarp();
-  int bad = 0;
+  int n_emit = 0, bad = 0;
   for (int base = 0; base < n_pos; base += 32) {
     const int i = base + lane;
     int r = -1;
     if (i < n_pos) r = recurrent ? i : (int)s.order[i];
-    const bool emit = r >= 0 && (s.flags[r] & 1) && !(s.flags[r] & 2) && s.needed[r];
-    const bool store = emit && (recurrent || s.used[r] || (s.flags[r] & 4));
-    const int cnt = emit ? s.in_start[r + 1] - s.in_start[r] : 0;
+    const bool emit = r >= 0 && (s.flags[r] & F_LIVE) && !(s.flags[r] & F_INPUT) && s.needed[r];
     const unsigned me = __ballot_sync(0xffffffffu, emit);
-    const unsigned ms = __ballot_sync(0xffffffffu, store);
-    const unsigned lt = (1u << lane) - 1;
-    int x = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, d);
-      if (lane >= d) x += y;
-    }
     if (emit) {
-      const int k = n_steps + __popc(me & lt);
-      const uint16_t slot = store ? (uint16_t)(I + n_store + __popc(ms & lt)) : NO_SLOT;
-      s.slot_of[r] = slot;
       const double* nr = gn + (int64_t)r * 5;
       const double av = nr[4], gv = nr[3];
       if (!(av >= 0.0 && av < ACT_COUNT && av == floor(av))) bad |= ST_BAD_ACT;
       if (!(gv >= 0.0 && gv < AGG_COUNT && gv == floor(gv))) bad |= ST_BAD_AGG;
-      StepT<T> st;
-      memset(&st, 0, sizeof(st));
-      st.slot = slot;
-      st.act = (uint8_t)(av >= 0.0 && av < ACT_COUNT ? (int)av : 0);
-      st.agg = (uint8_t)(gv >= 0.0 && gv < AGG_COUNT ? (int)gv : 0);
-      st.e_begin = (uint16_t)(n_edges + x - cnt);
-      st.e_count = (uint16_t)cnt;
-      st.bias = (T)nr[1];
-      st.resp = (T)nr[2];
-      steps[k] = st;
+      const int agg = (gv >= 0.0 && gv < AGG_COUNT) ? (int)gv : 0;
+      const uint64_t cls = (recurrent || !(agg == AGG_SUM || agg == AGG_MEAN)) ? 1 : 0;
+      const uint64_t cnt = (uint64_t)(s.in_start[r + 1] - s.in_start[r]);
+      const uint64_t lv = recurrent ? 0 : (uint64_t)s.lvl[r];
+      s.gkey[n_emit + __popc(me & ((1u << lane) - 1))] =
+          (lv << 48) | (cls << 47) | ((0xFFFFull - cnt) << 16) | (uint64_t)i;
     }
-    n_steps += __popc(me);
-    n_store += __popc(ms);
-    n_edges += __shfl_sync(0xffffffffu, x, 31);
+    n_emit += __popc(me);
   }
-  bad = __reduce_or_sync(0xffffffffu, bad);
-  status |= bad;
+  status |= __reduce_or_sync(0xffffffffu, bad);
+  const int Spad = next_pow2(n_emit);
+  for (int i = n_emit + lane; i < Spad; i += 32) s.gkey[i] = U64_MAX;
   __syncwarp();
+  warp_bitonic_sort(s.gkey, Spad);
 
-  // edges of each step (source slot + weight, source-row order); lanes own
-  // steps, each lane writes its step's edges
-  {
-    int kbase = 0;
-    for (int base = 0; base < n_pos; base += 32) {
-      const int i = base + lane;
-      int r = -1;
-      if (i < n_pos) r = recurrent ? i : (int)s.order[i];
-      const bool emit = r >= 0 && (s.flags[r] & 1) && !(s.flags[r] & 2) && s.needed[r];
-      const unsigned me = __ballot_sync(0xffffffffu, emit);
-      if (emit) {
-        const int k = kbase + __popc(me & ((1u << lane) - 1));
-        const int eb = steps[k].e_begin;
-        const int e0 = s.in_start[r], e1 = s.in_start[r + 1];
-        for (int e = e0; e < e1; ++e) {
-          const uint64_t kk = s.ekey[e];
-          const int sr = (int)((kk >> 32) & 0xFFFF);
-          const int crow = (int)(kk & 0xFFFFFFFFu);
-          EdgeT<T> ed;
-          memset(&ed, 0, sizeof(ed));
-          ed.src = s.slot_of[sr];
-          ed.w = (T)gc[(int64_t)crow * 4 + 3];
-          edges[eb + (e - e0)] = ed;
+  // group formation (sequential, lane 0): same level & class, <= 4 steps, and
+  // a step joins only if its list is at least half the group's longest list
+  // (bounds the padded edge entries, see edge_capacity)
+  if (lane == 0) {
+    int ng = 0, e_total = 0;
+    int cur_lv = -1, cur_cls = -1, cur_rounds = 0;
+    for (int k = 0; k < n_emit; ++k) {
+      const uint64_t key = s.gkey[k];
+      const int pos = (int)(key & 0xFFFF);
+      const int row = recurrent ? pos : (int)s.order[pos];
+      const int cnt = 0xFFFF - (int)((key >> 16) & 0xFFFF);
+      const int cls = (int)((key >> 47) & 1);
+      const int lv = (int)(key >> 48);
+      const bool join = ng > 0 && lv == cur_lv && cls == cur_cls && cls == 0 && s.grp[ng - 1].n < 4 &&
+                        2 * cnt >= cur_rounds;
+      if (!join) {
+        if (ng > 0) e_total = (int)align_up(e_total + group_width(s.grp[ng - 1].n) * s.grp[ng - 1].rounds, 8);
+        GroupRec gr;
+        memset(&gr, 0, sizeof(gr));
+        gr.cls = (uint8_t)cls; gr.rounds = (uint16_t)cnt;
+        gr.e_begin = (uint16_t)e_total; gr.step_begin = (uint16_t)k;
+        s.grp[ng++] = gr;
+        cur_lv = lv; cur_cls = cls; cur_rounds = cnt;
+      }
+      GroupRec& gr = s.grp[ng - 1];
+      gr.cnt[gr.n] = (uint16_t)cnt;
+      const bool tanh_sum = gn[(int64_t)row * 5 + 4] == (double)ACT_TANH && gn[(int64_t)row * 5 + 3] == (double)AGG_SUM;
+      if (gr.n == 0) gr.cls |= tanh_sum ? GRP_TANH_SUM : 0;
+      else if (!tanh_sum) gr.cls &= ~GRP_TANH_SUM;
+      gr.n++;
+      s.step_row[k] = (uint16_t)row;
+      s.grp_of[k] = (uint16_t)(ng - 1);
+    }
+    if (ng > 0) e_total = (int)align_up(e_total + group_width(s.grp[ng - 1].n) * s.grp[ng - 1].rounds, 8);
+    s.ready[0] = (uint32_t)ng;  // Kahn is done: ready/indeg serve as scalar mailboxes
+    s.indeg[0] = e_total;
+  }
+  __syncwarp();
+  const int n_groups = (int)s.ready[0];
+  const int e_total = s.indeg[0];
+
+  // ---- liveness: last group reading each node ---------------------------------
+  for (int r = lane; r < N; r += 32)
+    s.last_grp[r] = (recurrent || (s.flags[r] & F_OUTPUT)) ? NEVER : -1;
+  __syncwarp();
+  if (!recurrent) {
+    for (int k = lane; k < n_emit; k += 32) {
+      const int row = s.step_row[k];
+      const int gk = s.grp_of[k];
+      for (int e = s.in_start[row]; e < s.in_start[row + 1]; ++e)
+        atomicMax(&s.last_grp[(int)((s.ekey[e] >> 32) & 0xFFFF)], gk);
+    }
+  }
+  // slots: 0..I-1 hold the inputs, the rest start free
+  const int WS = (N + 2 + 31) / 32;
+  for (int w = lane; w < WS; w += 32) {
+    uint32_t m = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int sl = w * 32 + b;
+      if (sl >= I && sl < N + 2) m |= 1u << b;
+    }
+    s.freemask[w] = m;
+  }
+  for (int r = lane; r < N; r += 32)
+    if (s.flags[r] & F_INPUT) s.slot_of[r] = (uint16_t)gn[(int64_t)r * 5];
+  __syncwarp();
+  int n_slots = I;
+  for (int gi = 0; gi < n_groups; ++gi) {
+    // recycle the slots whose last reader is this group (reads precede writes)
+    if (!recurrent) {
+      for (int r = lane; r < N; r += 32) {
+        const uint16_t sl = s.slot_of[r];
+        if (sl != NO_SLOT && !(s.flags[r] & (F_OUTPUT | F_FREED)) && s.last_grp[r] <= gi) {
+          s.flags[r] |= F_FREED;
+          atomicOr(&s.freemask[sl >> 5], 1u << (sl & 31));
         }
       }
-      kbase += __popc(me);
+      __syncwarp();
+    }
+    const GroupRec gr = s.grp[gi];
+    for (int j = 0; j < gr.n; ++j) {
+      const int row = s.step_row[gr.step_begin + j];
+      if (!(s.used[row] || (s.flags[row] & F_OUTPUT))) continue;
+      const int sl = warp_first_set(s.freemask, WS);
+      __syncwarp();
+      if (lane == 0) {
+        s.freemask[sl >> 5] &= ~(1u << (sl & 31));
+        s.slot_of[row] = (uint16_t)sl;
+      }
+      n_slots = max(n_slots, sl + 1);
+      __syncwarp();
+    }
+  }
+  // ---- write groups, steps and interleaved edge lists --------------------------
+  GroupRec* pg = (GroupRec*)(gp + L.off_groups);
+  StepT<T>* steps = (StepT<T>*)(gp + L.off_steps);
+  for (int gi = lane; gi < n_groups; gi += 32) pg[gi] = s.grp[gi];
+  for (int k = lane; k < n_emit; k += 32) {
+    const int row = s.step_row[k];
+    const GroupRec gr = s.grp[s.grp_of[k]];
+    const int j = k - gr.step_begin, gw = group_width(gr.n);
+    const double* nr = gn + (int64_t)row * 5;
+    const double av = nr[4], gv = nr[3];
+    StepT<T> st;
+    memset(&st, 0, sizeof(st));
+    const int e0 = s.in_start[row], cnt = s.in_start[row + 1] - e0;
+    st.slot = (s.used[row] || (s.flags[row] & F_OUTPUT)) ? s.slot_of[row] : NO_SLOT;
+    st.act = (uint8_t)((av >= 0.0 && av < ACT_COUNT) ? (int)av : 0);
+    st.agg = (uint8_t)((gv >= 0.0 && gv < AGG_COUNT) ? (int)gv : 0);
+    st.count = (uint16_t)cnt;
+    st.bias = (T)nr[1];
+    st.resp = (T)nr[2];
+    steps[k] = st;
+    // column j of the group's edge block; holes (and the spare column of a
+    // 3-group) are zero entries that the kernels never read
+    const int ncol = (gr.n == 3 && j == 2) ? 2 : 1;
+    for (int col = j; col < j + ncol; ++col) {
+      for (int rr = 0; rr < gr.rounds; ++rr) {
+        const int idx = gr.e_begin + rr * gw + col;
+        uint32_t src = 0;
+        double w = 0.0;
+        if (col == j && rr < cnt) {
+          const uint64_t kk = s.ekey[e0 + rr];
+          src = s.slot_of[(int)((kk >> 32) & 0xFFFF)];
+          w = gc[(int64_t)(kk & 0xFFFFFFFFu) * 4 + 3];
+        }
+        if (sizeof(T) == 8) {
+          EdgeD ed;
+          ed.src = src; ed.pad = 0; ed.w = w;
+          ((EdgeD*)(gp + L.off_w))[idx] = ed;
+        } else {
+          ((uint16_t*)(gp + L.off_src))[idx] = (uint16_t)src;
+          ((float*)(gp + L.off_w))[idx] = (float)w;
+        }
+      }
     }
   }
   uint16_t* out_slot = (uint16_t*)(gp + L.off_out);
@@ -406,12 +528,12 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     out_slot[o] = r >= 0 ? s.slot_of[r] : NO_SLOT;
   }
   if (lane == 0) {
-    ProgHeader h{n_steps, n_edges, I + n_store, n_order, status, n_live, mode, 0};
+    ProgHeader h{n_emit, e_total, n_slots, n_order, status, n_live, mode, n_groups};
     *hdr = h;
     if (status_out) status_out[g] = status;
-    atomicMax(&maxdims[0], I + n_store);
-    atomicMax(&maxdims[1], n_steps);
-    atomicMax(&maxdims[2], n_edges);
+    atomicMax(&maxdims[0], n_slots);
+    atomicMax(&maxdims[1], n_emit);
+    atomicMax(&maxdims[2], e_total);
   }
 }
 
@@ -421,7 +543,7 @@ using namespace tneat;
 
 extern "C" {
 
-// Bytes of one genome's program (header + output slots + steps + edges).
+// Bytes of one genome's program (header + output slots + groups + steps + edges).
 int64_t an_program_stride(int N, int C, int O, int precision) {
   return prog_layout(N, C, O, precision).stride;
 }
@@ -431,19 +553,20 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
                  int mode, int precision, int prune, void* program, int64_t program_stride,
                  int16_t* order, int16_t* conn_rows, int32_t* io_rows, int32_t* status,
                  int32_t* maxdims, void* stream) {
-  if (P < 0 || N < 1 || N > 65535 || C < 0 || C > 65535 || I < 1 || O < 1 || I + O > N) return -1;
+  if (P < 0 || N < 1 || N > 32767 || C < 0 || edge_capacity(N, C) > 65535 || I < 1 || O < 1 || I + O > N)
+    return -1;
   if (!nodes || !program || !maxdims || (C > 0 && !conns)) return -2;
   const ProgLayout L = prog_layout(N, C, O, precision);
   if (program_stride != L.stride) return -3;
   if (P == 0) return 0;
-  const int64_t ws = warp_smem_bytes(N, C > 0 ? C : 1);
+  const int Cc = C > 0 ? C : 1;
+  const int64_t ws = warp_smem_bytes(N, Cc);
+  if (ws > 200 * 1024) return -4;  // genome capacity too large for one warp's shared memory
   int wpb = 4;
   while (wpb > 1 && ws * wpb > 160 * 1024) wpb >>= 1;
-  if (ws > 200 * 1024) return -4;  // genome capacity too large for one warp's shared memory
   const int64_t smem = ws * wpb;
   const int64_t blocks = (P + wpb - 1) / wpb;
   cudaStream_t st = (cudaStream_t)stream;
-  const int Cc = C > 0 ? C : 1;
   if (precision) {
     cudaFuncSetAttribute(transform_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     transform_kernel<double><<<(unsigned)blocks, 32 * wpb, smem, st>>>(
@@ -455,7 +578,6 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
         nodes, conns, P, N, C, I, O, mode, prune, ws, (uint8_t*)program, L, order, conn_rows,
         io_rows, status, maxdims);
   }
-  (void)Cc;
   TNEAT_CHECK_LAUNCH();
   return 0;
 }

@@ -217,7 +217,13 @@ def finalize_transform(stacked: StackedNetworks) -> np.ndarray:
     return the cyclic genome indices (feed-forward mode)."""
     md = stacked._cache.pop("maxdims_dev", None)
     if md is not None:
-        stacked.maxdims = tuple(int(v) for v in md.cpu().tolist())
+        # one read-back: launch sizes, per-genome status and value-slot counts
+        slots = stacked.program[:, 8:12].contiguous().view(torch.int32).reshape(-1)
+        host = torch.cat([md, stacked.status_dev, slots]).cpu().numpy()
+        p = stacked.size
+        stacked.maxdims = tuple(int(v) for v in host[:3])
+        stacked._cache["status"] = host[3:3 + p]
+        stacked._cache["slots"] = host[3 + p:]
     st = stacked.status
     hard = st & (ST_BAD_KEY | ST_DANGLING | ST_MISSING_IO)
     if hard.any():
@@ -274,11 +280,47 @@ def _check_codes(stacked: StackedNetworks) -> None:
         raise ConfigError(f"unknown {kind} code in genomes {which}")
 
 
+_TILE_TT = {1: 128, 2: 256, 3: 64, 4: 256, 5: 128, 6: 128}
+_SMEM_PER_SM = 228 * 1024
+
+
+def _bucket_plan(stacked: StackedNetworks, variant: int) -> list:
+    """Occupancy buckets: genomes sorted by value-slot count and split where
+    the number of resident CTAs per SM changes; each bucket is one launch with
+    its own (tighter) shared-memory size.  Cached on the stacked object."""
+    key = ("plan", variant)
+    if key in stacked._cache:
+        return stacked._cache[key]
+    tt = _TILE_TT[variant]
+    esz = 8 if stacked.precision else 4
+    slots = stacked._cache.get("slots")
+    if slots is None:
+        slots = stacked.program[:, 8:12].contiguous().view(torch.int32).reshape(-1).cpu().numpy()
+    order = np.argsort(slots, kind="stable").astype(np.int32)
+    sorted_slots = slots[order]
+    ids = torch.from_numpy(order).pin_memory().to(stacked.program.device, non_blocking=True)
+    _, ms, me = stacked.maxdims
+    prog = 32 * ms + (16 * me if stacked.precision else 6 * me + 16) + 16
+    pad = {1: 1, 2: 2, 3: 1, 4: 4, 5: 2, 6: 4}[variant]
+    occ = _SMEM_PER_SM // (prog + np.maximum(sorted_slots, stacked.num_inputs) * (tt + pad) * esz + 1024)
+    plan = []
+    lo = 0
+    n = sorted_slots.size
+    while lo < n:
+        hi = lo + int(np.searchsorted(occ[lo:] != occ[lo], True))  # first index with another class
+        hi = n if hi == lo else hi
+        plan.append((ids[lo:hi], (int(sorted_slots[hi - 1]), ms, me)))
+        lo = hi
+    stacked._cache[key] = plan
+    return plan
+
+
 def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Tensor | None = None,
-                   *, shared: bool = False, variant: int = 0,
+                   *, shared: bool = False, variant: int = 0, bucketed: bool = True,
                    stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """Device-resident forward: inputs (P,B,I) (or (B,I) with shared=True) on
-    the GPU in the program's dtype -> outputs (P,B,O).  No host syncs."""
+    the GPU in the program's dtype -> outputs (P,B,O).  No host syncs after
+    the first call on a given StackedNetworks (the bucket plan is cached)."""
     dt = _TORCH_DT[stacked.precision]
     if inputs.dtype != dt or not inputs.is_cuda or not inputs.is_contiguous():
         raise ValueError(f"inputs must be a contiguous CUDA {dt} tensor")
@@ -295,19 +337,28 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
         raise InvalidInput(f"expected input length {stacked.num_inputs}, got {i}")
     if out is None:
         out = torch.empty((pop, b, stacked.num_outputs), dtype=dt, device=inputs.device)
-    md = _maxdims_arg(stacked)
-    _native.call("an_forward", ptr(stacked.program), stacked.stride, stacked.max_nodes,
-                 stacked.max_conns, stacked.precision, md, ptr(inputs), gstride, pop, b, i,
-                 stacked.num_outputs, ptr(out), int(variant), stream_handle(stream))
+    v = (variant & 0xF) or (5 if b >= 192 else (3 if b >= 96 else 8))
+    args = (ptr(stacked.program), stacked.stride, stacked.max_nodes, stacked.max_conns, stacked.precision)
+    tail = (b, i, stacked.num_outputs, ptr(out), int(variant) if variant > 15 else int(v),
+            stream_handle(stream))
+    v &= 0xF
+    if v in _TILE_TT and bucketed and pop > 1:
+        for ids, md in _bucket_plan(stacked, v):
+            _native.call("an_forward", *args, _maxdims_arg(stacked, md), ptr(ids), ptr(inputs), gstride,
+                         int(ids.numel()), *tail)
+    else:
+        _native.call("an_forward", *args, _maxdims_arg(stacked), None, ptr(inputs), gstride, pop, *tail)
     return out
 
 
-def _maxdims_arg(stacked: StackedNetworks) -> int:
+def _maxdims_arg(stacked: StackedNetworks, dims=None) -> int:
     """Host int32[3] launch sizes, kept alive on the stacked object."""
-    arr = stacked._cache.get("maxdims_host")
-    if arr is None or tuple(arr) != tuple(stacked.maxdims):
-        arr = (ctypes.c_int32 * 3)(*[int(v) for v in stacked.maxdims])
-        stacked._cache["maxdims_host"] = arr
+    dims = tuple(int(v) for v in (dims or stacked.maxdims))
+    key = ("maxdims_host", dims)
+    arr = stacked._cache.get(key)
+    if arr is None:
+        arr = (ctypes.c_int32 * 3)(*dims)
+        stacked._cache[key] = arr
     return ctypes.addressof(arr)
 
 
