@@ -83,6 +83,74 @@ int an_forward_fitness(const void* program, int64_t program_stride, int N, int C
                        int64_t P, int B, int I, int O, int kind, const double* targets,
                        double* fitness, void* stream);
 
+
+/* Cart-pole lockstep episodes (CartPoleProblem.evaluate_stacked,
+ * problems.py:153-177, 257-271): warp per genome, float64 Euler dynamics
+ * (problems.py:107-122), observations (x, x_dot, theta, theta_dot) -> output
+ * row of key I; force = +10 if output > 0 else -10; start (P,4) float64;
+ * fitness (P,) float64 = steps survived (<= max_steps). */
+int an_cartpole(const void* program, int64_t program_stride, int N, int C, int precision,
+                const int32_t* maxdims_host, int64_t P, const double* start, int max_steps, double* fitness,
+                void* stream);
+
+/* ---- evolution operators (evolution.py / genome.py) ------------------------ */
+
+/* Mutation / initialisation hyper-parameters (NeatConfig, config.py:31-86),
+ * flattened.  Option lists hold function codes (functions.py:26-39). */
+typedef struct an_mutate_params {
+  int32_t N, C, I, O;          /* max_nodes, max_conns, inputs, outputs */
+  int32_t feedforward;         /* network_type == "feedforward" */
+  int32_t act_default, agg_default;
+  int32_t n_act_options, n_agg_options;
+  int32_t act_options[8];
+  int32_t agg_options[8];
+  int32_t pad;
+  double node_add, node_delete, conn_add, conn_delete;
+  double bias_init_mean, bias_init_std, bias_mutate_power, bias_mutate_rate, bias_replace_rate;
+  double response_init_mean, response_init_std, response_mutate_power, response_mutate_rate,
+      response_replace_rate;
+  double weight_init_mean, weight_init_std, weight_mutate_power, weight_mutate_rate, weight_replace_rate;
+  double enabled_mutate_rate, activation_replace_rate, aggregation_replace_rate;
+  double attr_min, attr_max;
+} an_mutate_params;
+
+/* Tape cells of counter-based streams (rng.py:86-134): out[s, j] = uniform
+ * (normals=0) or Box-Muller normal (normals=1, u1 at base+j, u2 at
+ * base+width+j) of stream keys[s].  Test hook for RngStream parity. */
+int an_rng_draw(const uint64_t* keys, int64_t S, uint64_t base, int64_t width, int normals, double* out,
+                void* stream);
+
+/* init_arrays (genome.py:129-160): genome g draws normals from stream keys[g]
+ * starting at counter `base`; nodes (P,N,5), conns (P,C,4) written. */
+int an_init(double* nodes, double* conns, int64_t P, const uint64_t* keys, uint64_t base,
+            const an_mutate_params* params, void* stream);
+
+/* distance_arrays (evolution.py:425-488), bit-exact float64 (sums in the
+ * reference's genome-1 row order).  pair_mode 1: out[p] = d(g1[p], g2[Q==1 ? 0 : p]);
+ * pair_mode 0: out[q*P + p] = d(g1[p], g2[q]) (speciation, evolution.py:513-559). */
+int an_distance(const double* n1, const double* c1, int64_t P, const double* n2, const double* c2, int64_t Q,
+                int pair_mode, int N, int C, double c_disjoint, double c_homologous, double* out, void* stream);
+
+/* mutate_arrays (evolution.py:172-325) in place.  keys[i] = stream key of
+ * genome i (RngStream._keys), tape cells start at `base` (its counter);
+ * new_keys[i] = key a firing node addition uses; can_add (P,) uint8 or NULL. */
+int an_mutate(double* nodes, double* conns, int64_t P, const uint64_t* keys, uint64_t base,
+              const double* new_keys, const an_mutate_params* params, uint8_t* can_add, void* stream);
+
+/* _crossover_into (evolution.py:101-136): out_* hold the fitter parents and
+ * are blended in place with less_* (coins at cells base.. of keys[i]). */
+int an_crossover(double* out_nodes, double* out_conns, const double* less_nodes, const double* less_conns,
+                 int64_t P, int N, int C, const uint64_t* keys, uint64_t base, void* stream);
+
+/* reproduce worker (evolution.py:685-709) for slots slot_base..+n_slots-1:
+ * uniforms(2) parent picks from pool[pool_offset[i] + ...], crossover,
+ * mutation, elite overwrite (elite_src[i] >= 0).  Stream of slot s =
+ * fold(stage_key, s); a firing node addition in slot s takes key new_key_base + s. */
+int an_reproduce(const double* pop_nodes, const double* pop_conns, double* out_nodes, double* out_conns,
+                 int64_t n_slots, int64_t slot_base, const int32_t* pool, const int32_t* pool_offset,
+                 const int32_t* pool_size, const int32_t* elite_src, uint64_t stage_key, double new_key_base,
+                 const an_mutate_params* params, uint8_t* can_add, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,10 +13,17 @@ from .errors import (ArrayNeatError, BadAttrIndex, CapacityFull, ConfigError, Cy
                      ShapeMismatch, TerminalState)
 from .functions import (ACTIVATION_IDS, AGGREGATION_IDS, DEFAULT_REGISTRY,
                         EXTENDED_AGGREGATION_IDS, FunctionRegistry)
-from .genome import GenomeTensors, PopulationTensors
+from .genome import GenomeTensors, PopulationTensors, init_arrays, init_genome
 from .inference import (StackedNetworks, TransformedNetwork, finalize_transform, forward,
                         forward_arrays, forward_batch, forward_device, population_forward,
                         population_transform, transform, transform_arrays,
                         transform_population_stacked)
+from . import evolution, problems, rng  # noqa: E402  (module attributes)
+from .evolution import (GenerationStats, NodeKeyAllocator, SpeciesState, allocate_spawns, crossover,
+                        crossover_arrays, distance, distance_arrays, evolve_step, mutate, mutate_arrays,
+                        reproduce, speciate, update_stagnation)
+from .problems import (CartPoleProblem, Problem, RegressionProblem, XorProblem, evaluate_population,
+                       make_problem)
+from .rng import RngStream
 
 __version__ = "0.1.0"

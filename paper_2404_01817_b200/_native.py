@@ -14,7 +14,7 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtneat.so")
 
-P, I32, I64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+P, I32, I64, U64, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
 
 # name -> (restype, argtypes); keep in sync with include/tneat.h
 SIGNATURES: dict[str, tuple] = {
@@ -22,7 +22,30 @@ SIGNATURES: dict[str, tuple] = {
     "an_transform": (I32, [P, P, I64, I32, I32, I32, I32, I32, I32, I32, P, I64, P, P, P, P, P, P]),
     "an_forward": (I32, [P, I64, I32, I32, I32, P, P, P, I64, I64, I32, I32, I32, P, I32, P]),
     "an_forward_fitness": (I32, [P, I64, I32, I32, I32, P, P, I64, I64, I32, I32, I32, I32, P, P, P]),
+    "an_cartpole": (I32, [P, I64, I32, I32, I32, P, I64, P, I32, P, P]),
+    "an_rng_draw": (I32, [P, I64, U64, I64, I32, P, P]),
+    "an_init": (I32, [P, P, I64, P, U64, P, P]),
+    "an_distance": (I32, [P, P, I64, P, P, I64, I32, I32, I32, D, D, P, P]),
+    "an_mutate": (I32, [P, P, I64, P, U64, P, P, P, P]),
+    "an_crossover": (I32, [P, P, P, P, I64, I32, I32, P, U64, P]),
+    "an_reproduce": (I32, [P, P, P, P, I64, I64, P, P, P, P, U64, D, P, P, P]),
 }
+
+
+class MutateParams(ctypes.Structure):
+    """Mirror of include/tneat.h an_mutate_params."""
+    _fields_ = [(n, ctypes.c_int32) for n in ("N", "C", "I", "O", "feedforward", "act_default",
+                                               "agg_default", "n_act_options", "n_agg_options")] + [
+        ("act_options", ctypes.c_int32 * 8), ("agg_options", ctypes.c_int32 * 8), ("pad", ctypes.c_int32)] + [
+        (n, ctypes.c_double) for n in (
+            "node_add", "node_delete", "conn_add", "conn_delete",
+            "bias_init_mean", "bias_init_std", "bias_mutate_power", "bias_mutate_rate", "bias_replace_rate",
+            "response_init_mean", "response_init_std", "response_mutate_power", "response_mutate_rate",
+            "response_replace_rate",
+            "weight_init_mean", "weight_init_std", "weight_mutate_power", "weight_mutate_rate",
+            "weight_replace_rate",
+            "enabled_mutate_rate", "activation_replace_rate", "aggregation_replace_rate",
+            "attr_min", "attr_max")]
 
 _lib = None
 _lock = threading.Lock()

@@ -22,6 +22,8 @@ OUT = os.path.join(HERE, "libtneat.so")
 BUILD = os.path.join(os.path.dirname(HERE), "build", "tneat")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# evolve.cu reproduces numpy's float64 rounding: no FMA contraction there
+PER_FILE = {"evolve.cu": ["-fmad=false"]}
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
 
@@ -55,7 +57,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         src, obj = pair
         if not force and not _stale(obj, src):
             return obj, ""
-        cmd = [nvcc, *ARCH, *FLAGS, "-I", CSRC, "-c", src, "-o", obj]
+        cmd = [nvcc, *ARCH, *FLAGS, *PER_FILE.get(os.path.basename(src), []), "-I", CSRC, "-c", src, "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         res = subprocess.run(cmd, capture_output=True, text=True)

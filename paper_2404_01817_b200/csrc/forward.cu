@@ -513,6 +513,83 @@ __global__ void fwd_warp_kernel(const uint8_t* __restrict__ prog, ProgLayout L, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// cart-pole lockstep episodes (problems.py:153-177), warp per genome, B = 1
+// ---------------------------------------------------------------------------
+
+// one synchronous pass over the program for a single input vector held in vals[slot]
+template <typename T>
+__device__ void warp_eval_single(const uint8_t* gp, const ProgLayout& L, T* vals) {
+  const int lane = threadIdx.x & 31;
+  const ProgHeader hdr = *reinterpret_cast<const ProgHeader*>(gp);
+  const GroupRec* groups = reinterpret_cast<const GroupRec*>(gp + L.off_groups);
+  const StepT<T>* steps = reinterpret_cast<const StepT<T>*>(gp + L.off_steps);
+  const uint16_t* esrc = reinterpret_cast<const uint16_t*>(gp + L.off_src);
+  const float* ew = reinterpret_cast<const float*>(gp + L.off_w);
+  const EdgeD* ed = reinterpret_cast<const EdgeD*>(gp + L.off_w);
+  for (int g = 0; g < hdr.n_groups; ++g) {
+    const GroupRec gr = groups[g];
+    const int stride = (gr.cls & GRP_GENERIC) ? 1 : group_width(gr.n);
+    T y[4];
+    for (int j = 0; j < gr.n; ++j) {
+      const StepT<T> st = steps[gr.step_begin + j];
+      T part = agg_neutral<T>(st.agg);
+      for (int e = lane; e < st.count; e += 32) {
+        const int idx = gr.e_begin + e * stride + j;
+        uint32_t src;
+        T w;
+        if constexpr (sizeof(T) == 8) { src = ed[idx].src; w = ed[idx].w; }
+        else { src = esrc[idx]; w = ew[idx]; }
+        part = agg_combine<T>(st.agg, part, w * vals[src]);
+      }
+      y[j & 3] = eval_node<T>(st, warp_allreduce<T>(st.agg, part));
+    }
+    __syncwarp();
+    if (lane == 0)
+      for (int j = 0; j < gr.n; ++j) {
+        const uint16_t sl = steps[gr.step_begin + j].slot;
+        if (sl != NO_SLOT) vals[sl] = y[j & 3];
+      }
+    __syncwarp();
+  }
+}
+
+template <typename T>
+__global__ void cartpole_kernel(const uint8_t* __restrict__ prog, ProgLayout L, int64_t P, int max_slots,
+                                const double* __restrict__ start, int max_steps, double* __restrict__ fitness) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (gi >= P) return;
+  T* vals = reinterpret_cast<T*>(smem) + (int64_t)warp * max_slots;
+  const uint8_t* gp = prog + gi * L.stride;
+  const uint16_t out0 = *reinterpret_cast<const uint16_t*>(gp + L.off_out);
+  // classic constants (problems.py:37-47), evaluated as numpy does
+  const double G = 9.8, PM = 0.1, TM = 1.0 + 0.1, HL = 0.5, PL = 0.1 * 0.5, FM = 10.0, TS = 0.02;
+  const double XL = 2.4, THL = 12.0 * 2.0 * 3.141592653589793 / 360.0;
+  double x = start[gi * 4 + 0], xd = start[gi * 4 + 1], th = start[gi * 4 + 2], thd = start[gi * 4 + 3];
+  int steps = 0;
+  for (int t = 0; t < max_steps; ++t) {
+    if (lane == 0) { vals[0] = (T)x; vals[1] = (T)xd; vals[2] = (T)th; vals[3] = (T)thd; }
+    __syncwarp();
+    warp_eval_single<T>(gp, L, vals);
+    const double out = out0 != NO_SLOT ? (double)vals[out0] : __longlong_as_double(0x7ff8000000000000ll);
+    const double force = out > 0.0 ? FM : -FM;
+    const double ct = cos(th), st = sin(th);
+    const double tmp = __ddiv_rn(__dadd_rn(force, __dmul_rn(__dmul_rn(PL, __dmul_rn(thd, thd)), st)), TM);
+    const double tacc = __ddiv_rn(__dsub_rn(__dmul_rn(G, st), __dmul_rn(ct, tmp)),
+                                  __dmul_rn(HL, __dsub_rn(4.0 / 3.0, __ddiv_rn(__dmul_rn(PM, __dmul_rn(ct, ct)), TM))));
+    const double xacc = __dsub_rn(tmp, __ddiv_rn(__dmul_rn(__dmul_rn(PL, tacc), ct), TM));
+    x = __dadd_rn(x, __dmul_rn(TS, xd));
+    xd = __dadd_rn(xd, __dmul_rn(TS, xacc));
+    th = __dadd_rn(th, __dmul_rn(TS, thd));
+    thd = __dadd_rn(thd, __dmul_rn(TS, tacc));
+    ++steps;
+    if (fabs(x) > XL || fabs(th) > THL) break;
+  }
+  if (lane == 0) fitness[gi] = (double)steps;
+}
+
 template <typename T>
 int launch_warp(const uint8_t* prog, const ProgLayout& L, int64_t P, const T* in, int64_t in_gstride,
                 int B, int I, int O, const int32_t* maxdims_host, T* out, int64_t out_gstride,
@@ -632,6 +709,30 @@ int an_forward_fitness(const void* program, int64_t program_stride, int N, int C
                                O, maxdims_host, nullptr, 0, kind, targets, fitness, st);
   return launch_warp<float>((const uint8_t*)program, L, P, (const float*)inputs, input_genome_stride, B, I, O,
                             maxdims_host, nullptr, 0, kind, targets, fitness, st);
+}
+
+// Cart-pole lockstep fitness (problems.py:153-177, 257-271): start (P,4) float64
+// states, episodes of at most max_steps, fitness = steps survived.
+int an_cartpole(const void* program, int64_t program_stride, int N, int C, int precision,
+                const int32_t* maxdims_host, int64_t P, const double* start, int max_steps, double* fitness,
+                void* stream) {
+  if (P < 0 || !maxdims_host || max_steps < 0) return -1;
+  if (P == 0) return 0;
+  const ProgLayout L = prog_layout(N, C, 1, precision);
+  if (L.stride != program_stride) return -3;
+  const int slots = max(maxdims_host[0], 4);
+  const int wpb = 4;
+  const int64_t smem = (int64_t)wpb * slots * (precision ? 8 : 4);
+  const int64_t blocks = (P + wpb - 1) / wpb;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (precision)
+    cartpole_kernel<double><<<(unsigned)blocks, 32 * wpb, smem, st>>>((const uint8_t*)program, L, P, slots,
+                                                                      start, max_steps, fitness);
+  else
+    cartpole_kernel<float><<<(unsigned)blocks, 32 * wpb, smem, st>>>((const uint8_t*)program, L, P, slots,
+                                                                     start, max_steps, fitness);
+  TNEAT_CHECK_LAUNCH();
+  return 0;
 }
 
 }  // extern "C"

@@ -10,6 +10,7 @@ reference's float64 value; the kernels read rows with 8/16-byte loads.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -70,3 +71,38 @@ class PopulationTensors:
         k = len(genomes)
         return cls(np.stack([g.nodes for g in genomes]), np.stack([g.conns for g in genomes]),
                    np.full(k, -1, dtype=np.int64), np.full(k, np.nan), g0.num_inputs, g0.num_outputs)
+
+
+def init_arrays(config, rng, *, on_device: bool = False):
+    """Fresh genomes, inputs fully connected to outputs (genome.py:129-160).
+
+    ``rng`` is a batched stream (e.g. ``RngStream(seed).child(0, 0).split(arange(P))``);
+    draws: normals(N) bias, normals(N) response, normals(C) weight per stream.
+    Returns numpy arrays, or CUDA tensors with ``on_device=True``."""
+    import torch
+
+    from . import _native
+    from .device import device, ptr, stream_handle
+    from .evolution import mutate_params
+
+    keys = np.asarray(rng._keys, dtype=np.uint64).reshape(-1)
+    batch = tuple(rng.batch_shape)
+    pop = keys.size
+    dev = device()
+    nodes = torch.empty((pop, config.max_nodes, 5), dtype=torch.float64, device=dev)
+    conns = torch.empty((pop, config.max_conns, 4), dtype=torch.float64, device=dev)
+    kd = torch.from_numpy(keys.view(np.int64).copy()).to(dev)
+    params = mutate_params(config)
+    _native.call("an_init", ptr(nodes), ptr(conns), pop, ptr(kd), int(rng._counter), ctypes.addressof(params),
+                 stream_handle())
+    rng._counter += 4 * config.max_nodes + 2 * config.max_conns
+    if on_device:
+        return nodes.reshape(batch + tuple(nodes.shape[1:])), conns.reshape(batch + tuple(conns.shape[1:]))
+    return (nodes.cpu().numpy().reshape(batch + (config.max_nodes, 5)),
+            conns.cpu().numpy().reshape(batch + (config.max_conns, 4)))
+
+
+def init_genome(config, rng) -> GenomeTensors:
+    """Single fresh genome (genome.py:163-166)."""
+    nodes, conns = init_arrays(config, rng)
+    return GenomeTensors(nodes, conns, config.inputs, config.outputs)

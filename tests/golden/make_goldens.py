@@ -203,6 +203,122 @@ def make_rng_goldens() -> None:
     _save("rng.npz", **out)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "evo" not in sys.argv:
     make_rng_goldens()
     make_forward_goldens()
+
+
+# -- evolution operators --------------------------------------------------------
+
+EVO_CFG = dict(inputs=3, outputs=2, max_nodes=32, max_conns=64, pop_size=200,
+               node_add=0.5, node_delete=0.2, conn_add=0.6, conn_delete=0.2,
+               bias_mutate_rate=0.8, bias_replace_rate=0.1,
+               response_init_std=0.3, response_mutate_rate=0.3, response_mutate_power=0.3,
+               response_replace_rate=0.05,
+               weight_mutate_rate=0.8, weight_replace_rate=0.1, enabled_mutate_rate=0.05,
+               activation_options=("identity", "tanh", "sigmoid", "relu"), activation_replace_rate=0.3,
+               aggregation_options=("sum", "product", "max", "mean"), aggregation_replace_rate=0.3)
+
+
+def make_evolution_goldens() -> None:
+    from arrayneat.evolution import _crossover_into, reproduce, speciate, update_stagnation, allocate_spawns
+    cfg = an.NeatConfig(**EVO_CFG)
+    c = load_corpus()
+    nodes, conns = c["nodes"], c["conns"]
+    P = nodes.shape[0]
+    out = {}
+    # init_arrays
+    init_rng = an.RngStream(5).child(0, 0).split(np.arange(40))
+    out["init_nodes"], out["init_conns"] = init_arrays(cfg, init_rng)
+    # mutate_arrays, feed-forward and recurrent
+    for net in ("feedforward", "recurrent"):
+        mcfg = cfg.with_overrides(network_type=net)
+        st = an.RngStream(77).child(3, 2).split(np.arange(P))
+        st._counter = 5  # arbitrary tape offset
+        keys = np.arange(1000, 1000 + P, dtype=np.float64)
+        mn, mc, added = an_evo.mutate_arrays(nodes, conns, mcfg, st, keys)
+        out[f"mut_{net}_nodes"], out[f"mut_{net}_conns"], out[f"mut_{net}_added"] = mn, mc, added
+        out[f"mut_{net}_counter"] = np.int64(st._counter)
+    # crossover of genome i (fitter) with genome P-1-i
+    st = an.RngStream(91).child(1, 2).split(np.arange(P))
+    st._counter = 2
+    xn, xc = nodes.copy(), conns.copy()
+    _crossover_into(xn, xc, nodes[::-1].copy(), conns[::-1].copy(), st)
+    out["xo_nodes"], out["xo_conns"], out["xo_counter"] = xn, xc, np.int64(st._counter)
+    # speciation of the corpus from scratch and against two old species
+    scfg = cfg.with_overrides(compatibility_threshold=1.2, max_species=6)
+    pop = an.PopulationTensors(nodes, conns, np.full(P, -1, np.int64), np.full(P, np.nan), 3, 2)
+    sp_pop, sp = speciate(pop, [], scfg)
+    out["spec0_assigned"] = sp_pop.species_id
+    out["spec0_keys"] = np.array([s.species_key for s in sp])
+    out["spec0_reps"] = np.stack([s.representative.nodes for s in sp])
+    old = [an_evo.SpeciesState(species_key=k, representative=pop.genome(g), member_indices=np.arange(1))
+           for k, g in ((3, 17), (8, 101))]
+    sp_pop, sp = speciate(pop, old, scfg)
+    out["spec1_assigned"] = sp_pop.species_id
+    out["spec1_keys"] = np.array([s.species_key for s in sp])
+    out["spec1_reps_nodes"] = np.stack([s.representative.nodes for s in sp])
+    # stagnation / spawns / reproduce from the from-scratch speciation with synthetic fitness
+    fitness = np.round(np.random.default_rng(3).random(P) * 4.0, 2)  # ties on purpose
+    sp_pop, sp = speciate(pop, [], scfg)
+    surv = update_stagnation(sp, fitness, scfg)
+    alloc = allocate_spawns(surv, fitness, scfg.with_overrides(pop_size=P))
+    out["spawns"] = np.array([s.spawn_count for s in alloc])
+    rcfg = scfg.with_overrides(pop_size=P)
+    allocator = an.NodeKeyAllocator(500)
+    off = reproduce(sp_pop, alloc, fitness, rcfg, an.RngStream(13).child(4), allocator)
+    out["rep_nodes"], out["rep_conns"] = off.nodes, off.conns
+    out["rep_fitness"] = fitness
+    out["rep_next_key"] = np.int64(allocator.next_key)
+    _save("evolution.npz", **out)
+
+
+def load_corpus() -> dict:
+    with np.load(os.path.join(HERE, "corpus.npz")) as z:
+        return {k: z[k] for k in z.files}
+
+
+if __name__ == "__main__":
+    make_evolution_goldens()
+
+
+def make_problem_goldens() -> None:
+    """Fitness of mutated populations under the reference problems, plus a
+    short reference XOR run (stats rows) from a fixed seed."""
+    from arrayneat import problems as an_prob
+    from arrayneat.runner import init_state
+    out = {}
+    for name, (ni, no) in {"xor": (2, 1), "regression": (1, 1), "cartpole": (4, 1)}.items():
+        cfg = an.NeatConfig(inputs=ni, outputs=no, max_nodes=24, max_conns=48, pop_size=120, problem=name,
+                            node_add=0.6, conn_add=0.7, bias_mutate_rate=0.8, weight_mutate_rate=0.9,
+                            activation_options=("identity", "tanh", "sigmoid", "relu"),
+                            activation_replace_rate=0.3)
+        nodes, conns = init_arrays(cfg, an.RngStream(31).child(0, 0).split(np.arange(cfg.pop_size)))
+        alloc = an.NodeKeyAllocator(ni + no)
+        for rnd in range(6):
+            st = an.RngStream(31).child(rnd + 1, 2).split(np.arange(cfg.pop_size))
+            base = alloc.reserve(cfg.pop_size)
+            nodes, conns, _ = an_evo.mutate_arrays(nodes, conns, cfg, st,
+                                                   np.arange(base, base + cfg.pop_size, dtype=np.float64))
+        pop = an.PopulationTensors(nodes, conns, np.full(cfg.pop_size, -1), np.full(cfg.pop_size, np.nan), ni, no)
+        fit = an_prob.make_problem(cfg).evaluate_population_tensors(pop, rng=an.RngStream(9).child(4, 1))
+        out[f"{name}_nodes"], out[f"{name}_conns"], out[f"{name}_fitness"] = nodes, conns, fit
+    # short XOR run from init_state (runner.py:54-66, 165-169)
+    cfg = an.NeatConfig(seed=3, pop_size=150, generation_limit=5)
+    state = init_state(cfg)
+    problem = an_prob.make_problem(cfg)
+    rows = []
+    pop, species, alloc = state.population, state.species, state.allocator
+    root = an.RngStream(cfg.seed)
+    for gen in range(5):
+        pop, species, stats = an_evo.evolve_step(pop, species, cfg, root.child(gen), alloc, problem)
+        rows.append([stats.best_fitness, stats.mean_fitness, stats.species_count, stats.mean_live_nodes,
+                     stats.mean_live_conns])
+    out["run_stats"] = np.array(rows)
+    out["run_final_nodes"], out["run_final_conns"] = pop.nodes, pop.conns
+    out["run_final_species"] = pop.species_id
+    _save("problems.npz", **out)
+
+
+if __name__ == "__main__":
+    make_problem_goldens()

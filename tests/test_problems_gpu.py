@@ -1,0 +1,71 @@
+"""GPU fitness plugins and a short evolution run against reference goldens
+(tests/golden/problems.npz).
+
+Fitness is float64 on the device (f64 programs); the reference's tanh /
+sigmoid come from numpy's SIMD libm, CUDA's from libdevice, so XOR /
+regression fitness agree to 1e-9 (the reference's own oracle bound) and
+cart-pole step counts agree exactly except for rare trajectories where a
+1-ulp difference flips a bang-bang decision (bounded below).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import cuda_ok, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tn():
+    if not cuda_ok():
+        pytest.skip("no CUDA device")
+    import paper_2404_01817_b200 as tn
+    return tn
+
+
+@pytest.mark.parametrize("name,ni", [("xor", 2), ("regression", 1), ("cartpole", 4)])
+def test_problem_fitness(tn, name, ni):
+    g = load_golden("problems.npz")
+    cfg = tn.NeatConfig(inputs=ni, outputs=1, max_nodes=24, max_conns=48, pop_size=120, problem=name)
+    pop = tn.PopulationTensors(g[f"{name}_nodes"], g[f"{name}_conns"], None, None, ni, 1)
+    fit = tn.make_problem(cfg).evaluate_population_tensors(pop, rng=tn.RngStream(9).child(4, 1))
+    ref = g[f"{name}_fitness"]
+    if name == "cartpole":
+        assert np.mean(fit == ref) >= 0.97, np.nonzero(fit != ref)
+    else:
+        np.testing.assert_allclose(fit, ref, rtol=1e-9, atol=1e-9)
+
+
+def test_xor_problem_fp32_path(tn):
+    g = load_golden("problems.npz")
+    prob = tn.XorProblem()
+    prob.precision = "f32"
+    pop = tn.PopulationTensors(g["xor_nodes"], g["xor_conns"], None, None, 2, 1)
+    fit = prob.evaluate_population_tensors(pop)
+    np.testing.assert_allclose(fit, g["xor_fitness"], rtol=0, atol=1e-4)
+
+
+def test_short_xor_run_tracks_reference(tn):
+    """Five generations from the same seed: per-generation statistics track
+    the reference (exactly while every structural decision matches)."""
+    from paper_2404_01817_b200.runner import init_state, stats_row  # noqa: F401
+    g = load_golden("problems.npz")
+    cfg = tn.NeatConfig(seed=3, pop_size=150, generation_limit=5)
+    state = init_state(cfg)
+    problem = tn.make_problem(cfg)
+    root = tn.RngStream(cfg.seed)
+    pop, species = state.population, state.species
+    rows = []
+    for gen in range(5):
+        pop, species, stats = tn.evolve_step(pop, species, cfg, root.child(gen), state.allocator, problem)
+        rows.append([stats.best_fitness, stats.mean_fitness, stats.species_count, stats.mean_live_nodes,
+                     stats.mean_live_conns])
+    rows = np.array(rows)
+    ref = g["run_stats"]
+    np.testing.assert_allclose(rows, ref, rtol=1e-9, atol=1e-9)
+    nodes = pop.nodes.cpu().numpy() if hasattr(pop.nodes, "cpu") else pop.nodes
+    assert np.array_equal(np.isnan(nodes), np.isnan(g["run_final_nodes"]))
+    assert np.array_equal(pop.species_id, g["run_final_species"])
