@@ -151,6 +151,16 @@ int an_reproduce(const double* pop_nodes, const double* pop_conns, double* out_n
                  const int32_t* pool_size, const int32_t* elite_src, uint64_t stage_key, double new_key_base,
                  const an_mutate_params* params, uint8_t* can_add, void* stream);
 
+/* ---- HyperNEAT (builder-defined; no reference implementation) ---- */
+
+/* Substrate fitness on the tensor cores (tcgen05 kind::tf32, TMEM
+ * accumulators, fused tanh / squared-error epilogue): W (P,64,64) fp32 CPPN
+ * weights (row = output node), X (S,64) fp32 shared substrate inputs (S a
+ * multiple of 128), target (S,) fp32; fitness (P,) float64 =
+ * -mean((tanh(X W_p^T) - target[:,None])^2). */
+int an_substrate_fitness(const float* W, int64_t P, const float* X, const float* target, int S, double* fitness,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -340,3 +340,24 @@ def synthetic_population(pop: int, max_nodes: int, max_conns: int, num_inputs: i
         conns[p, crow, CEN] = (rng.random(e) < 0.9).astype(np.float64)
         conns[p, crow, CW] = np.clip(rng.standard_normal(e), -30, 30)
     return nodes, conns
+
+
+# -- HyperNEAT restatement (no reference: SPEC.md:8; parity UNPINNED beyond the
+# CPPN query, which is forward_genome on coordinate inputs) ----------------------
+
+
+def substrate_query_inputs(grid: int = 8) -> np.ndarray:
+    """q = k*n + j -> (x_j, y_j, x_k, y_k) on an grid x grid lattice over [-1,1]^2."""
+    lin = np.linspace(-1.0, 1.0, grid)
+    pts = [(lin[c], lin[r]) for r in range(grid) for c in range(grid)]
+    n = len(pts)
+    return np.array([[pts[j][0], pts[j][1], pts[k][0], pts[k][1]] for k in range(n) for j in range(n)])
+
+
+def substrate_fitness(nodes: np.ndarray, conns: np.ndarray, x: np.ndarray, t: np.ndarray) -> float:
+    """W = CPPN(queries) (forward_genome, float64); fitness = -mean((tanh(X W^T) - t)^2)."""
+    tr = transform_genome(nodes, conns, 4, 1)
+    q = substrate_query_inputs()
+    w = forward_genome(nodes, tr, q)[:, 0].reshape(64, 64)
+    y = np.tanh(x.astype(np.float64) @ w.T)
+    return float(-np.mean((y - t.astype(np.float64)[:, None]) ** 2))

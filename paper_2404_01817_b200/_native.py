@@ -29,6 +29,7 @@ SIGNATURES: dict[str, tuple] = {
     "an_mutate": (I32, [P, P, I64, P, U64, P, P, P, P]),
     "an_crossover": (I32, [P, P, P, P, I64, I32, I32, P, U64, P]),
     "an_reproduce": (I32, [P, P, P, P, I64, I64, P, P, P, P, U64, D, P, P, P]),
+    "an_substrate_fitness": (I32, [P, I64, P, P, I32, P, P]),
 }
 
 
@@ -74,7 +75,11 @@ def lib() -> ctypes.CDLL:
 
 
 def call(name: str, *args) -> int:
-    """Invoke ``name`` and raise NativeError on a negative status."""
+    """Invoke ``name`` and raise NativeError on a negative status.  Only
+    entry points with a declared ctypes signature may be called (an
+    undeclared one would be called with C-int arguments)."""
+    if name not in SIGNATURES:
+        raise NativeError(f"{name} has no ctypes signature in _native.SIGNATURES")
     ret = getattr(lib(), name)(*args)
     if ret < 0:
         if ret <= -100:

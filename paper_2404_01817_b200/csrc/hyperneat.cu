@@ -1,0 +1,266 @@
+// K9: HyperNEAT substrate evaluation on the 5th-generation tensor cores.
+//
+// No reference implementation exists; semantics are
+// builder-defined and documented in DESIGN.md:
+//   * each genome's CPPN is queried on the 64 x 64 (output node, input node)
+//     grid of an 8x8 -> 8x8 substrate (forward kernel, shared inputs) giving
+//     W_p (64 x 64, row = output node k, column = input node j);
+//   * substrate batch X (S x 64, S = multiple of 128) is shared by all genomes;
+//     Y_p = tanh(X W_p^T), fitness_p = -mean_{s,k} (Y_p[s,k] - t[s])^2.
+//
+// This is the only dense contraction of the system, so it is the one kernel on
+// tcgen05: each CTA owns 4 genomes (N = 4 x 64 = 256 accumulator columns),
+// their W rows are the B operand (K-major, staged once); the CTA streams
+// 128-row tiles of X as the A operand through two shared-memory buffers
+// (cp.async), one elected thread issues `tcgen05.mma.kind::tf32` (M=128,
+// N=256, K=8 per instruction, 8 per tile) into one of two TMEM accumulators
+// (2 x 256 columns), and the four warps run the fused epilogue (tcgen05.ld ->
+// tanh -> squared error -> running sum) of tile t-1 while the tensor core
+// works on tile t.  Y is never written to memory.
+
+#include "common.cuh"
+
+namespace tneat {
+
+constexpr int HN_K = 64;           // substrate inputs
+constexpr int HN_N1 = 64;          // substrate outputs per genome
+constexpr int HN_G = 4;            // genomes per CTA
+constexpr int HN_N = HN_N1 * HN_G; // MMA N
+constexpr int HN_M = 128;          // rows per tile (MMA M)
+constexpr int HN_THREADS = 128;
+
+// K-major, no-swizzle canonical layout (cute UMMA INTERLEAVE): 8-row x 16-byte
+// core matrices; inside a block of 8 rows the 16 K-chunks (4 fp32 each) are
+// 128 B apart (LBO), consecutive 8-row blocks are 2048 B apart (SBO).
+__device__ __forceinline__ uint32_t km_offset(int row, int k) {
+  return (uint32_t)((row >> 3) * 2048 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);       // start address
+  d |= (uint64_t)(128 >> 4) << 16;              // leading byte offset (K direction)
+  d |= (uint64_t)(2048 >> 4) << 32;             // stride byte offset (M/N direction)
+  d |= (uint64_t)1 << 46;                       // descriptor version (sm_100)
+  return d;                                     // base offset 0, layout SWIZZLE_NONE
+}
+
+// kind::tf32, D = F32, A = B = TF32, both K-major, N = 256, M = 128
+constexpr uint32_t HN_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(HN_N >> 3) << 17) |
+                              ((uint32_t)(HN_M >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+#define TMEM_LD16(taddr, r)                                                                              \
+  asm volatile(                                                                                          \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, " \
+      "[%16];"                                                                                           \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),       \
+        "=r"(r[15])                                                                                      \
+      : "r"(taddr))
+
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct __align__(1024) HnSmem {
+  float b[HN_N * HN_K];          // 64 KB: 4 genomes' W rows, K-major core matrices
+  float a[2][HN_M * HN_K];       // 2 x 32 KB: X tiles
+  float part[HN_THREADS / 32][HN_G];
+  uint64_t mma_bar[2];
+  uint32_t tmem_base;
+};
+
+// stage one 128 x 64 fp32 tile of X (rows r0..r0+127) into the core-matrix layout
+__device__ __forceinline__ void load_a_tile(float* a, const float* __restrict__ X, int r0) {
+  const uint32_t base = smem_u32(a);
+  for (int c = threadIdx.x; c < HN_M * HN_K / 4; c += HN_THREADS) {
+    const int row = c >> 4, k = (c & 15) * 4;
+    cp_async16(base + km_offset(row, k), X + (int64_t)(r0 + row) * HN_K + k);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(HN_THREADS, 1)
+substrate_kernel(const float* __restrict__ W, int64_t P, const float* __restrict__ X,
+                 const float* __restrict__ target, int S, double* __restrict__ fitness) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  HnSmem& sm = *reinterpret_cast<HnSmem*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t g0 = (int64_t)blockIdx.x * HN_G;
+  const int ng = (int)(P - g0 < HN_G ? P - g0 : HN_G);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&sm.tmem_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(smem_u32(&sm.mma_bar[0]), 1);
+    mbar_init(smem_u32(&sm.mma_bar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // B operand: rows n = g*64 + k (output node k of genome g), K = input node j
+  {
+    const uint32_t base = smem_u32(sm.b);
+    for (int c = tid; c < HN_N * HN_K / 4; c += HN_THREADS) {
+      const int row = c >> 4, k = (c & 15) * 4;
+      const int g = row >> 6;
+      if (g < ng) {
+        cp_async16(base + km_offset(row, k), W + ((g0 + g) * HN_N1 + (row & 63)) * (int64_t)HN_K + k);
+      } else {
+        float* dst = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sm.b) + km_offset(row, k));
+        dst[0] = dst[1] = dst[2] = dst[3] = 0.f;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  load_a_tile(sm.a[0], X, 0);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_base;
+  const int tiles = S / HN_M;
+  float acc_err[HN_G] = {0.f, 0.f, 0.f, 0.f};
+  uint32_t phase[2] = {0u, 0u};
+
+  auto epilogue = [&](int tile, int stage) {
+    // thread = tile row; TMEM lane = 32 * (warp % 4) + lane
+    const float tv = target[(int64_t)tile * HN_M + tid];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(stage * HN_N);
+#pragma unroll
+    for (int g = 0; g < HN_G; ++g) {
+#pragma unroll 1
+      for (int q = 0; q < HN_N1 / 16; ++q) {
+        uint32_t r[16];
+        TMEM_LD16(taddr + g * HN_N1 + q * 16, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float d = tanh_approx(__uint_as_float(r[i])) - tv;
+          acc_err[g] = fmaf(d, d, acc_err[g]);
+        }
+      }
+    }
+  };
+
+  for (int t = 0; t < tiles; ++t) {
+    const int stage = t & 1;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async data -> tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // A[t] (and B) staged; epilogue(t-2) done with accumulator `stage`
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0) {
+      const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b);
+#pragma unroll
+      for (int kk = 0; kk < HN_K / 8; ++kk)  // K = 8 tf32 per instruction = 2 core matrices
+        mma_tf32(tmem + (uint32_t)(stage * HN_N), smem_desc(a0 + kk * 256), smem_desc(b0 + kk * 256), HN_IDESC,
+                 kk > 0 ? 1u : 0u);
+      mma_commit(smem_u32(&sm.mma_bar[stage]));
+    }
+    if (t >= 1) {
+      // MMA t-1 finished -> its A buffer (the other one) is free and its accumulator ready
+      mbar_wait(smem_u32(&sm.mma_bar[stage ^ 1]), phase[stage ^ 1]);
+      phase[stage ^ 1] ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (t + 1 < tiles) load_a_tile(sm.a[stage ^ 1], X, (t + 1) * HN_M);
+      epilogue(t - 1, stage ^ 1);
+    } else if (t + 1 < tiles) {
+      // the other A buffer has never been used
+      load_a_tile(sm.a[stage ^ 1], X, (t + 1) * HN_M);
+    }
+  }
+  {
+    const int last = tiles - 1, stage = last & 1;
+    mbar_wait(smem_u32(&sm.mma_bar[stage]), phase[stage]);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    epilogue(last, stage);
+  }
+  // reduce squared errors over the CTA's 128 rows
+#pragma unroll
+  for (int g = 0; g < HN_G; ++g) {
+    float v = acc_err[g];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if (lane == 0) sm.part[warp][g] = v;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid < ng) {
+    double s = 0.0;
+    for (int w = 0; w < HN_THREADS / 32; ++w) s += (double)sm.part[w][tid];
+    fitness[g0 + tid] = -s / ((double)S * HN_N1);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+}  // namespace tneat
+
+using namespace tneat;
+
+extern "C" {
+
+// HyperNEAT substrate fitness (builder-defined): W (P,64,64) fp32
+// CPPN weights (row = output node), X (S,64) fp32 shared substrate inputs
+// (S a multiple of 128), target (S,) fp32; fitness (P,) float64 =
+// -mean((tanh(X W_p^T) - target[:,None])^2).  tcgen05 kind::tf32 MMAs.
+int an_substrate_fitness(const float* W, int64_t P, const float* X, const float* target, int S, double* fitness,
+                         void* stream) {
+  if (P < 0 || S <= 0 || S % HN_M != 0) return -1;
+  if (P == 0) return 0;
+  if (!W || !X || !target || !fitness) return -2;
+  const int smem = (int)sizeof(HnSmem) + 1024;
+  cudaFuncSetAttribute(substrate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int64_t blocks = (P + HN_G - 1) / HN_G;
+  substrate_kernel<<<(unsigned)blocks, HN_THREADS, smem, (cudaStream_t)stream>>>(W, P, X, target, S, fitness);
+  TNEAT_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // extern "C"
