@@ -151,6 +151,17 @@ int an_reproduce(const double* pop_nodes, const double* pop_conns, double* out_n
                  const int32_t* pool_size, const int32_t* elite_src, uint64_t stage_key, double new_key_base,
                  const an_mutate_params* params, uint8_t* can_add, void* stream);
 
+/* ---- recurrent rollouts (builder-defined; the reference rejects recurrent
+ * genomes) ---------------------------------------------------- */
+
+/* Fixed-step synchronous recurrent evaluation inside s' = tanh(A s + M a):
+ * program compiled with an_transform mode 1; A (D,D), M (D,O), s0 (D,) in the
+ * program's precision; per environment step the inputs are clamped to s and
+ * `sweeps` synchronous sweeps run; fitness (P,) float64 = sum_t s_t[0]. */
+int an_rollout(const void* program, int64_t program_stride, int N, int C, int precision,
+               const int32_t* maxdims_host, int64_t P, int I, int O, const void* A, const void* M, const void* s0,
+               int D, int steps, int sweeps, double* fitness, void* stream);
+
 /* ---- HyperNEAT (builder-defined; no reference implementation) ---- */
 
 /* Substrate fitness on the tensor cores (tcgen05 kind::tf32, TMEM

@@ -361,3 +361,37 @@ def substrate_fitness(nodes: np.ndarray, conns: np.ndarray, x: np.ndarray, t: np
     w = forward_genome(nodes, tr, q)[:, 0].reshape(64, 64)
     y = np.tanh(x.astype(np.float64) @ w.T)
     return float(-np.mean((y - t.astype(np.float64)[:, None]) ** 2))
+
+
+# -- recurrent restatement (no reference: SPEC.md:360 rejects recurrent
+# genomes; parity UNPINNED) -------------------------------------------------------
+
+
+def recurrent_rollout(nodes: np.ndarray, conns: np.ndarray, num_inputs: int, num_outputs: int,
+                      a: np.ndarray, m: np.ndarray, s0: np.ndarray, steps: int, sweeps: int) -> float:
+    """K synchronous sweeps per environment step over the enabled graph
+    (cycles allowed), node math of inference.py:217-253; s' = tanh(A s + M a)."""
+    rows = key_to_row(nodes)
+    into: dict[int, list[tuple[int, float]]] = {}
+    for s_, d_, w_, _ in enabled_edges(nodes, conns):
+        into.setdefault(d_, []).append((s_, w_))
+    in_rows = [rows[k] for k in range(num_inputs)]
+    out_rows = [rows[k] for k in range(num_inputs, num_inputs + num_outputs)]
+    hidden = [r for r in live_rows(nodes) if r not in set(in_rows)]
+    v = {r: 0.0 for r in live_rows(nodes)}
+    s = np.asarray(s0, dtype=np.float64).copy()
+    reward = 0.0
+    for _ in range(steps):
+        reward += float(s[0])
+        for i, r in enumerate(in_rows):
+            v[r] = float(s[i]) if i < s.size else 0.0
+        for _ in range(sweeps):
+            new = {}
+            for r in hidden:
+                terms = [np.array([w * v[src]]) for src, w in sorted(into.get(r, []))]
+                agg = agg_apply(int(nodes[r, AGG]), terms, 1)[0]
+                new[r] = float(act_apply(int(nodes[r, ACT]), np.array([nodes[r, BIAS] + nodes[r, RESP] * agg]))[0])
+            v.update(new)
+        act = np.array([v[r] for r in out_rows])
+        s = np.tanh(a @ s + m @ act)
+    return reward

@@ -30,6 +30,7 @@ SIGNATURES: dict[str, tuple] = {
     "an_crossover": (I32, [P, P, P, P, I64, I32, I32, P, U64, P]),
     "an_reproduce": (I32, [P, P, P, P, I64, I64, P, P, P, P, U64, D, P, P, P]),
     "an_substrate_fitness": (I32, [P, I64, P, P, I32, P, P]),
+    "an_rollout": (I32, [P, I64, I32, I32, I32, P, I64, I32, I32, P, P, P, I32, I32, I32, P, P]),
 }
 
 
