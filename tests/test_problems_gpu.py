@@ -69,3 +69,26 @@ def test_short_xor_run_tracks_reference(tn):
     nodes = pop.nodes.cpu().numpy() if hasattr(pop.nodes, "cpu") else pop.nodes
     assert np.array_equal(np.isnan(nodes), np.isnan(g["run_final_nodes"]))
     assert np.array_equal(pop.species_id, g["run_final_species"])
+
+
+def test_sharded_generation_single_rank_equals_evolve_step(tn):
+    """The sharded generation (distributed.py) on one rank reproduces
+    evolve_step exactly (same kernels, same RNG tape)."""
+    import numpy as np
+    from paper_2404_01817_b200.distributed import Collective, DeviceOps, sharded_evolve_step
+    from paper_2404_01817_b200.runner import init_state
+    cfg = tn.NeatConfig(seed=5, pop_size=200, compatibility_threshold=2.0)
+    a = init_state(cfg)
+    b = init_state(cfg)
+    problem = tn.make_problem(cfg)
+    root = tn.RngStream(cfg.seed)
+    comm, ops = Collective(), DeviceOps(cfg)
+    pop, species = a.population, a.species
+    nodes, conns, lo, sp_b = b.population.nodes, b.population.conns, 0, b.species
+    for gen in range(3):
+        pop, species, st_a = tn.evolve_step(pop, species, cfg, root.child(gen), a.allocator, problem)
+        nodes, conns, lo, sp_b, st_b = sharded_evolve_step(nodes, conns, lo, sp_b, cfg, root.child(gen),
+                                                           b.allocator, problem, comm, ops)
+        assert st_a.best_fitness == st_b.best_fitness and st_a.mean_fitness == st_b.mean_fitness
+    assert np.array_equal(pop.nodes.cpu().numpy(), nodes.cpu().numpy(), equal_nan=True)
+    assert [s.species_key for s in species] == [s.species_key for s in sp_b]
