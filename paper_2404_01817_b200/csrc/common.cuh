@@ -84,7 +84,27 @@ template <> struct __align__(16) StepT<double> {
 // arrays, u16 source slots and f32 weights (6 bytes per edge)
 struct __align__(16) EdgeD { uint32_t src; uint32_t pad; double w; };
 
+// Split layout (format bit FMT_SPLIT, fp32 only): the inputs live in TMEM
+// columns (column = input key) and only hidden values take shared-memory slots;
+// each group keeps two interleaved edge blocks -- input-sourced edges (sources
+// are TMEM columns) and hidden-sourced edges (sources are hidden slots).
+struct __align__(16) GroupSplit {  // 32 bytes
+  uint8_t n;
+  uint8_t cls;
+  uint16_t rounds_in;
+  uint16_t rounds_h;
+  uint16_t step_begin;
+  uint16_t e_in;       // first entry of the input-edge block (multiple of 8)
+  uint16_t e_h;        // first entry of the hidden-edge block (multiple of 8)
+  uint16_t pad[2];
+  uint16_t cnt_in[4];
+  uint16_t cnt_h[4];
+};
+
+enum : int { FMT_F64 = 1, FMT_SPLIT = 2 };
+
 static_assert(sizeof(GroupRec) == 16, "group layout");
+static_assert(sizeof(GroupSplit) == 32, "group layout");
 static_assert(sizeof(StepT<float>) == 16, "step layout");
 static_assert(sizeof(StepT<double>) == 32, "step layout");
 static_assert(sizeof(EdgeD) == 16, "edge layout");
@@ -95,18 +115,22 @@ __host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + 
 // (a step joins a group only if its list is >= half the longest, so padded
 // <= 8/3 x real) and starts on a multiple of 8
 __host__ __device__ inline int64_t edge_capacity(int N, int C) { return 3ll * C + 8ll * N + 16; }
+// split layout: two padded blocks per group (each <= 2x its real entries) + alignment
+__host__ __device__ inline int64_t edge_capacity_split(int N, int C) { return 4ll * C + 16ll * N + 16; }
 
 struct ProgLayout {
   int64_t off_out, off_groups, off_steps, off_src, off_w, stride;
 };
 
+// `precision` is the program format: bit 0 = fp64 program, bit 1 = split layout (fp32)
 __host__ __device__ inline ProgLayout prog_layout(int N, int C, int O, int precision) {
   ProgLayout L;
-  const int64_t E = edge_capacity(N, C);
+  const bool split = (precision & FMT_SPLIT) != 0;
+  const int64_t E = split ? edge_capacity_split(N, C) : edge_capacity(N, C);
   L.off_out = 32;
   L.off_groups = align_up(L.off_out + 2 * (int64_t)O, 16);
-  L.off_steps = align_up(L.off_groups + 16ll * N, 16);
-  if (precision) {
+  L.off_steps = align_up(L.off_groups + (split ? 32ll : 16ll) * N, 16);
+  if (precision & FMT_F64) {
     L.off_src = align_up(L.off_steps + 32ll * N, 16);
     L.off_w = L.off_src;  // EdgeD pairs
     L.stride = align_up(L.off_w + 16 * E, 16);

@@ -23,6 +23,8 @@
 // activated; node = act(bias + response * agg(w * v)); empty aggregation = 0;
 // mean divides by the incoming count; outputs read at the rows of keys I..I+O-1.
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace tneat {
@@ -139,12 +141,17 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint16_t
     }
   }
   if constexpr (TANH) {
+    // tanh(b + r*a) = 2 / (1 + 2^(k (b + r*a))) - 1, k = -2 log2(e): one FFMA into
+    // EX2 (k folded into b and r once per step), FADD, RCP, FFMA -- |err| <~ 2e-7
+    constexpr float K = -2.8853900817779268f;
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       const StepT<float> sj = st[j];
+      const float rk = sj.resp * K, bk = sj.bias * K;
       PackT y;
 #pragma unroll
-      for (int s = 0; s < S; ++s) y.v[s] = tanh_fast(fmaf(sj.resp, acc[j][s], sj.bias));
+      for (int s = 0; s < S; ++s)
+        y.v[s] = fmaf(2.0f, rcp_approx(1.0f + ex2_approx(fmaf(rk, acc[j][s], bk))), -1.0f);
       if (sj.slot != NO_SLOT) *reinterpret_cast<PackT*>(vb + sj.slot * RB) = y;
     }
   } else {
@@ -291,17 +298,27 @@ __global__ void __launch_bounds__(NT, 1) fwd_tile_kernel(const uint8_t* __restri
   const T* gin = in + gi * in_gstride;
   T* go = out + gi * out_gstride;
   char* vb = reinterpret_cast<char*>(vals) + tid * S * sizeof(T);
+  uint32_t osl[8];
+  bool fast_out = sizeof(T) == 4 && O == 8;
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    osl[o] = oslot[o];
+    fast_out = fast_out && osl[o] != NO_SLOT;
+  }
   const int tile_end = min((run + 1) * tpc, (B + TT - 1) / TT);
   const bool vec_in = sizeof(T) == 4 && (I & 3) == 0 && (in_gstride & 3) == 0;
   const int step_s = (4 * NT) / I, step_i = (4 * NT) - step_s * I;  // chunk stride in (sample, input)
   const int step_s1 = NT / I, step_i1 = NT - step_s1 * I;
+  const int cps = I >> 2;
+  const int cps_shift = (cps & (cps - 1)) == 0 ? __ffs(cps) - 1 : -1;
+  const int cps_mask = cps - 1;
   // inputs -> value slots 0..I-1 (input key i lives in slot i).  A tile's
   // (samples x I) block is contiguous in HBM: it is read with coalesced 16-byte
   // loads and scattered into the [slot][sample] layout (rows padded by S
   // elements, so a warp's scattered stores hit distinct banks).  The next
   // tile's chunks are prefetched into registers while this tile computes, so
   // the HBM latency is off the critical path.
-  constexpr int PFMAX = 4 * S;
+  constexpr int PFMAX = 4 * S;  // register prefetch only when S * I / 4 <= 4 * S (I <= 16)
   const bool prefetch = vec_in && S * I / 4 <= PFMAX;
   const int per_thread = S * I / 4;
   float4 pf[PFMAX];
@@ -330,14 +347,22 @@ __global__ void __launch_bounds__(NT, 1) fwd_tile_kernel(const uint8_t* __restri
     if (tile != run * tpc) __syncthreads();  // previous tile fully consumed
     if (prefetch) {
       const int n4 = nt * I / 4;
-      int sm = (4 * tid) / I, i = 4 * tid - sm * I;
+      if (cps_shift >= 0) {  // I/4 chunks per input row is a power of two
 #pragma unroll
-      for (int k = 0; k < PFMAX; ++k) {
-        const int c = tid + k * NT;
-        if (k < per_thread && c < n4) TNEAT_SCATTER4(sm, i, pf[k]);
-        i += step_i;
-        sm += step_s;
-        if (i >= I) { i -= I; ++sm; }
+        for (int k = 0; k < PFMAX; ++k) {
+          const int c = tid + k * NT;
+          if (k < per_thread && c < n4) TNEAT_SCATTER4(c >> cps_shift, (c & cps_mask) << 2, pf[k]);
+        }
+      } else {
+        int sm = (4 * tid) / I, i = 4 * tid - sm * I;
+#pragma unroll
+        for (int k = 0; k < PFMAX; ++k) {
+          const int c = tid + k * NT;
+          if (k < per_thread && c < n4) TNEAT_SCATTER4(sm, i, pf[k]);
+          i += step_i;
+          sm += step_s;
+          if (i >= I) { i -= I; ++sm; }
+        }
       }
       if (tile + 1 < tile_end) TNEAT_ISSUE(tile + 1);
     } else if (vec_in) {
@@ -367,28 +392,38 @@ __global__ void __launch_bounds__(NT, 1) fwd_tile_kernel(const uint8_t* __restri
     // node sweep, one group of independent same-level nodes at a time
 #pragma unroll 1
     for (int g = 0; g < n_groups; ++g) {
-      const GroupRec gr = gr_s[g];
+      const uint4 raw = reinterpret_cast<const uint4*>(gr_s)[g];  // one LDS.128
+      GroupRec gr;
+      gr.n = (uint8_t)(raw.x & 0xFF);
+      gr.cls = (uint8_t)((raw.x >> 8) & 0xFF);
+      gr.rounds = (uint16_t)(raw.x >> 16);
+      gr.e_begin = (uint16_t)(raw.y & 0xFFFF);
+      gr.step_begin = (uint16_t)(raw.y >> 16);
+      gr.cnt[0] = (uint16_t)(raw.z & 0xFFFF);
+      gr.cnt[1] = (uint16_t)(raw.z >> 16);
+      gr.cnt[2] = (uint16_t)(raw.w & 0xFFFF);
+      gr.cnt[3] = (uint16_t)(raw.w >> 16);
       run_group<T, S, RB>(gr, src_s, w_s, ed_s, st_s + gr.step_begin, vb);
     }
 
-    // outputs (P, B, O)
+    // outputs (P, B, O): one S-wide load per output slot, 16-byte stores per input
+    if (fast_out) {
+      PackT v[8];
 #pragma unroll
-    for (int j = 0; j < S; ++j) {
-      const int s = s0 + j;
-      if (s >= B) break;
-      T y[8];
+      for (int o = 0; o < 8; ++o) v[o] = *reinterpret_cast<const PackT*>(vb + osl[o] * RB);
 #pragma unroll
-      for (int o = 0; o < 8; ++o)
-        y[o] = o < O ? (oslot[o] != NO_SLOT ? *reinterpret_cast<const T*>(vb + oslot[o] * RB + j * sizeof(T)) : T(NAN)) : T(0);
-      T* row = go + (int64_t)s * O;
-      if (sizeof(T) == 4 && O == 8) {
-        reinterpret_cast<float4*>(row)[0] = make_float4(y[0], y[1], y[2], y[3]);
-        reinterpret_cast<float4*>(row)[1] = make_float4(y[4], y[5], y[6], y[7]);
-      } else if (O <= 8) {
+      for (int j = 0; j < S; ++j) {
+        if (s0 + j >= B) break;
+        float4* row = reinterpret_cast<float4*>(go + (int64_t)(s0 + j) * 8);
+        row[0] = make_float4(v[0].v[j], v[1].v[j], v[2].v[j], v[3].v[j]);
+        row[1] = make_float4(v[4].v[j], v[5].v[j], v[6].v[j], v[7].v[j]);
+      }
+    } else {
 #pragma unroll
-        for (int o = 0; o < 8; ++o)
-          if (o < O) row[o] = y[o];
-      } else {
+      for (int j = 0; j < S; ++j) {
+        const int s = s0 + j;
+        if (s >= B) break;
+        T* row = go + (int64_t)s * O;
         for (int o = 0; o < O; ++o) {
           const uint16_t sl = __ldg(os + o);
           row[o] = sl != NO_SLOT ? *reinterpret_cast<const T*>(vb + sl * RB + j * sizeof(T)) : T(NAN);
@@ -628,7 +663,8 @@ int launch_tile(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, co
   const int64_t ms = maxdims_host[1], me = maxdims_host[2];
   const int64_t prog_bytes = ms * sizeof(GroupRec) + ms * sizeof(StepT<T>) +
                              (sizeof(T) == 8 ? 16 * me : align_up(2 * me, 16) + 4 * me);
-  const int64_t smem = align_up(prog_bytes, 16) + (int64_t)max(maxdims_host[0], I) * (TT + S) * sizeof(T);
+  int64_t smem = align_up(prog_bytes, 16) + (int64_t)max(maxdims_host[0], I) * (TT + S) * sizeof(T);
+  if (const char* pad = getenv("TNEAT_EXPERIMENT_SMEM_PAD")) smem += atoll(pad);  // occupancy experiments only
   if (smem > 227 * 1024) return -6;
   cudaFuncSetAttribute(fwd_tile_kernel<T, S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fwd_tile_kernel<T, S, NT><<<(unsigned)grid, NT, smem, st>>>(prog, L, ids, in, in_gstride, B, I, O, runs, tpc,
