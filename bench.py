@@ -61,6 +61,9 @@ def _parse():
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled every 50 ms during the timed
+    region, in-process through NVML (no nvidia-smi child competing for the
+    driver); falls back to `nvidia-smi -lms` when NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -70,8 +73,19 @@ class ClockSampler:
         self.samples: list[tuple[float, list[str]]] = []
         self.proc = None
         self.thread = None
+        self.stop_evt = threading.Event()
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:  # noqa: BLE001 -- fall back to the CLI
+            h = None
+        if h is not None:
+            self.thread = threading.Thread(target=self._nvml, args=(h,), daemon=True)
+            self.thread.start()
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -82,11 +96,27 @@ class ClockSampler:
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
 
+    def _nvml(self, h):
+        import pynvml
+        bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self.stop_evt.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:  # noqa: BLE001
+                break
+            self.samples.append((time.perf_counter(), [str(sm), str(mx)] +
+                                 ["Active" if r & b else "Not Active" for b in bits]))
+            self.stop_evt.wait(0.05)
+
     def _read(self):
         for line in self.proc.stdout:
             self.samples.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
 
     def stop(self):
+        self.stop_evt.set()
         if self.proc:
             self.proc.terminate()
             try:
@@ -271,6 +301,7 @@ def run_ours(args, rank: int, world: int) -> None:
     hdr = st.program[:, :32].contiguous().view(torch.int32).to(torch.int64).cpu().numpy()
     # header + output slots + groups + steps + edge entries (common.cuh layout)
     prog_bytes = int((32 + 16 + 16 * hdr[:, 7] + 16 * hdr[:, 0] + 6 * hdr[:, 1]).sum())
+    launches_per_step = 1 + len(tn.inference._bucket_plan(st, (args.variant & 0xF) or 5))
     algo_bytes = pop * BATCH * 4 * (NIN + NOUT) + prog_bytes
     fwd_avg = statistics.mean(fwd_ms) / 1e3
     peak, peak_kind = _peaks()
@@ -319,7 +350,7 @@ def run_ours(args, rank: int, world: int) -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(CONFIG, parallelism=f"population shards x{world} (no data-path collective)"),
             "e2e": e2e,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _ncu_traffic(),
                          "kernel": "fwd_tile_kernel", "algo_bytes_per_launch": algo_bytes,

@@ -4,7 +4,7 @@
 // into a fixed-stride "program" that the forward kernels (forward.cu) execute.
 // A program is a flat byte block per genome:
 //
-//   [ProgHeader 32 B][out_slot u16 x O][GroupRec x N][Step x N][edges x (3C+8N+16)]
+//   [ProgHeader 32 B][out_slot u16 x O][GroupRec x N][Step x N][edges x (3C+12N+16)]
 //
 // Steps are the non-input nodes that can influence an output (ancestor-cone
 // pruning, SURVEY.md App. B "K2 ... safe optimisation"), ordered by
@@ -40,7 +40,7 @@ constexpr uint16_t NO_SLOT = 0xFFFF;
 struct ProgHeader {  // 32 bytes
   int32_t n_steps;   // evaluated (non-input, needed) nodes
   int32_t n_edges;   // edge entries, including padding
-  int32_t n_slots;   // value slots (inputs first)
+  int32_t n_slots;   // value slots (inputs first; the last one is the zero slot)
   int32_t n_order;   // nodes placed in the Kahn order
   int32_t status;    // ST_* bits
   int32_t n_live;    // live node rows
@@ -52,10 +52,12 @@ struct ProgHeader {  // 32 bytes
 // with the same aggregation class.  Their edge lists are interleaved
 // round-major with a row width of gw = (n == 3 ? 4 : n) entries -- edge r of
 // step j sits at e_begin + r*gw + j -- so the forward kernel accumulates the n
-// nodes in lock-step as n independent FMA chains; entries past a step's count
-// are holes, skipped by a (warp-uniform) predicate.  e_begin is a multiple of
-// 8, so two rounds of sources / weights are single 16-byte loads.  Non-sum
-// aggregations are singleton groups.
+// nodes in lock-step as n independent FMA chains.  Sum/mean groups have an
+// even number of rounds; entries past a step's count are holes that read the
+// genome's zero slot (header n_slots - 1, never written) with weight 0, so the
+// rounds run unpredicated.  e_begin is a multiple of 8, so two rounds of
+// sources / weights are single 16-byte loads.  Non-sum aggregations are
+// singleton groups with exact counts.
 struct __align__(16) GroupRec {  // 16 bytes
   uint8_t n;           // steps in the group (1..4)
   uint8_t cls;         // GRP_* bits: GRP_GENERIC = non-sum aggregation (singleton),
@@ -113,8 +115,9 @@ __host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + 
 
 // edge entries a genome may need: each group's list is padded to gw*rounds
 // (a step joins a group only if its list is >= half the longest, so padded
-// <= 8/3 x real) and starts on a multiple of 8
-__host__ __device__ inline int64_t edge_capacity(int N, int C) { return 3ll * C + 8ll * N + 16; }
+// <= 8/3 x real), rounds are even (+gw <= 4 per group) and every group starts
+// on a multiple of 8 (+7)
+__host__ __device__ inline int64_t edge_capacity(int N, int C) { return 3ll * C + 12ll * N + 16; }
 // split layout: two padded blocks per group (each <= 2x its real entries) + alignment
 __host__ __device__ inline int64_t edge_capacity_split(int N, int C) { return 4ll * C + 16ll * N + 16; }
 

@@ -89,8 +89,8 @@ __device__ __forceinline__ void load_f32(const float* p, float (&out)[N]) {
 // One sum/mean group of G steps (fp32 program): edge block of width GW = G|4,
 // two rounds per iteration (2*GW sources in one <=16-byte load, weights in
 // <=2 16-byte loads) and up to 2G independent value loads / FMA chains.
-// Rounds below the shortest list run unpredicated; the tail skips holes with
-// warp-uniform predicates.  TANH: every step is tanh/sum (short epilogue).
+// All rounds run unpredicated (holes are zero-slot entries).  TANH: every
+// step is tanh/sum (short epilogue).
 template <int S, int G, int RB, bool TANH>
 __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint16_t* __restrict__ src_s,
                                               const float* __restrict__ w_s,
@@ -104,11 +104,9 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint16_t
     for (int s = 0; s < S; ++s) acc[j][s] = 0.0f;
   const uint16_t* sp = src_s + gr.e_begin;
   const float* wp = w_s + gr.e_begin;
-  const int rounds = gr.rounds;
-  const int full = gr.cnt[G - 1] & ~1;  // every step has an edge in rounds < full
-  int r = 0;
+  const int rounds = gr.rounds;  // even; holes read the zero slot with weight 0
 #pragma unroll 1
-  for (; r < full; r += 2) {
+  for (int r = 0; r < rounds; r += 2) {
     uint32_t sl[2 * GW];
     float w[2 * GW];
     load_u16<2 * GW>(sp + r * GW, sl);
@@ -123,22 +121,6 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint16_t
 #pragma unroll
         for (int s = 0; s < S; ++s) acc[q % GW][s] = fmaf(w[q], v[q].v[s], acc[q % GW][s]);
       }
-  }
-  if (r < rounds) {
-    int cnt[G];
-#pragma unroll
-    for (int j = 0; j < G; ++j) cnt[j] = gr.cnt[j];
-    for (; r < rounds; ++r) {
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        if (r < cnt[j]) {
-          const PackT v = *reinterpret_cast<const PackT*>(vb + (uint32_t)sp[r * GW + j] * RB);
-          const float w = wp[r * GW + j];
-#pragma unroll
-          for (int s = 0; s < S; ++s) acc[j][s] = fmaf(w, v.v[s], acc[j][s]);
-        }
-      }
-    }
   }
   if constexpr (TANH) {
     // tanh(b + r*a) = 2 / (1 + 2^(k (b + r*a))) - 1, k = -2 log2(e): one FFMA into
@@ -293,6 +275,9 @@ __global__ void __launch_bounds__(NT, 1) fwd_tile_kernel(const uint8_t* __restri
   const uint16_t* os = reinterpret_cast<const uint16_t*>(gp + L.off_out);
   __shared__ uint16_t oslot[8];
   if (tid < 8) oslot[tid] = tid < O ? __ldg(os + tid) : NO_SLOT;
+  // zero slot (last slot): read by padding entries, never written
+  if (hdr.n_slots > 0)
+    for (int i = tid; i < TT + S; i += NT) vals[(int64_t)(hdr.n_slots - 1) * (RB / sizeof(T)) + i] = T(0);
   __syncthreads();
 
   const T* gin = in + gi * in_gstride;

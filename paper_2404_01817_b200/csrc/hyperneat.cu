@@ -19,6 +19,7 @@
 // works on tile t.  Y is never written to memory.
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace tneat {
 
@@ -29,74 +30,12 @@ constexpr int HN_N = HN_N1 * HN_G; // MMA N
 constexpr int HN_M = 128;          // rows per tile (MMA M)
 constexpr int HN_THREADS = 128;
 
-// K-major, no-swizzle canonical layout (cute UMMA INTERLEAVE): 8-row x 16-byte
-// core matrices; inside a block of 8 rows the 16 K-chunks (4 fp32 each) are
-// 128 B apart (LBO), consecutive 8-row blocks are 2048 B apart (SBO).
-__device__ __forceinline__ uint32_t km_offset(int row, int k) {
-  return (uint32_t)((row >> 3) * 2048 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
-}
+// K-major, no-swizzle canonical layout (tc.cuh): 16 K-chunks per 8-row block,
+// consecutive 8-row blocks 2048 B apart
+constexpr uint32_t HN_SBO = 2048;
+__device__ __forceinline__ uint32_t km_offset(int row, int k) { return kmajor_offset(row, k, HN_SBO); }
 
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);       // start address
-  d |= (uint64_t)(128 >> 4) << 16;              // leading byte offset (K direction)
-  d |= (uint64_t)(2048 >> 4) << 32;             // stride byte offset (M/N direction)
-  d |= (uint64_t)1 << 46;                       // descriptor version (sm_100)
-  return d;                                     // base offset 0, layout SWIZZLE_NONE
-}
-
-// kind::tf32, D = F32, A = B = TF32, both K-major, N = 256, M = 128
-constexpr uint32_t HN_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(HN_N >> 3) << 17) |
-                              ((uint32_t)(HN_M >> 4) << 24);
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(bar),
-      "r"(phase)
-      : "memory");
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
-}
-
-#define TMEM_LD16(taddr, r)                                                                              \
-  asm volatile(                                                                                          \
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, " \
-      "[%16];"                                                                                           \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), \
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),       \
-        "=r"(r[15])                                                                                      \
-      : "r"(taddr))
+constexpr uint32_t HN_IDESC = idesc_tf32(HN_M, HN_N);
 
 __device__ __forceinline__ float tanh_approx(float x) {
   float y;
@@ -197,7 +136,7 @@ substrate_kernel(const float* __restrict__ W, int64_t P, const float* __restrict
       const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b);
 #pragma unroll
       for (int kk = 0; kk < HN_K / 8; ++kk)  // K = 8 tf32 per instruction = 2 core matrices
-        mma_tf32(tmem + (uint32_t)(stage * HN_N), smem_desc(a0 + kk * 256), smem_desc(b0 + kk * 256), HN_IDESC,
+        mma_tf32(tmem + (uint32_t)(stage * HN_N), smem_desc(a0 + kk * 256, HN_SBO), smem_desc(b0 + kk * 256, HN_SBO), HN_IDESC,
                  kk > 0 ? 1u : 0u);
       mma_commit(smem_u32(&sm.mma_bar[stage]));
     }

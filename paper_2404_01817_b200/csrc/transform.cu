@@ -404,7 +404,8 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
         if (ng > 0) e_total = (int)align_up(e_total + group_width(s.grp[ng - 1].n) * s.grp[ng - 1].rounds, 8);
         GroupRec gr;
         memset(&gr, 0, sizeof(gr));
-        gr.cls = (uint8_t)cls; gr.rounds = (uint16_t)cnt;
+        // sum/mean groups: even rounds (two per unrolled iteration), holes read the zero slot
+        gr.cls = (uint8_t)cls; gr.rounds = (uint16_t)(cls == 0 ? (cnt + 1) & ~1 : cnt);
         gr.e_begin = (uint16_t)e_total; gr.step_begin = (uint16_t)k;
         s.grp[ng++] = gr;
         cur_lv = lv; cur_cls = cls; cur_rounds = cnt;
@@ -438,7 +439,8 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
         atomicMax(&s.last_grp[(int)((s.ekey[e] >> 32) & 0xFFFF)], gk);
     }
   }
-  // slots: 0..I-1 hold the inputs, the rest start free
+  // slots: 0..I-1 hold the inputs, the rest start free; one more slot after
+  // the last allocated one is the zero slot read by padding entries
   const int WS = (N + 2 + 31) / 32;
   for (int w = lane; w < WS; w += 32) {
     uint32_t m = 0;
@@ -478,6 +480,8 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       __syncwarp();
     }
   }
+  const uint32_t zero_slot = (uint32_t)n_slots;
+  n_slots += 1;
   // ---- write groups, steps and interleaved edge lists --------------------------
   GroupRec* pg = (GroupRec*)(gp + L.off_groups);
   StepT<T>* steps = (StepT<T>*)(gp + L.off_steps);
@@ -499,12 +503,12 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     st.resp = (T)nr[2];
     steps[k] = st;
     // column j of the group's edge block; holes (and the spare column of a
-    // 3-group) are zero entries that the kernels never read
+    // 3-group) are (zero slot, 0.0) entries
     const int ncol = (gr.n == 3 && j == 2) ? 2 : 1;
     for (int col = j; col < j + ncol; ++col) {
       for (int rr = 0; rr < gr.rounds; ++rr) {
         const int idx = gr.e_begin + rr * gw + col;
-        uint32_t src = 0;
+        uint32_t src = zero_slot;
         double w = 0.0;
         if (col == j && rr < cnt) {
           const uint64_t kk = s.ekey[e0 + rr];

@@ -298,7 +298,7 @@ def _bucket_plan(stacked: StackedNetworks, variant: int) -> list:
         slots = stacked.program[:, 8:12].contiguous().view(torch.int32).reshape(-1).cpu().numpy()
     order = np.argsort(slots, kind="stable").astype(np.int32)
     sorted_slots = slots[order]
-    ids = torch.from_numpy(order).pin_memory().to(stacked.program.device, non_blocking=True)
+    ids = torch.from_numpy(order).to(stacked.program.device)  # 4P bytes; no pinned allocation per plan
     _, ms, me = stacked.maxdims
     prog = 32 * ms + (16 * me if stacked.precision else 6 * me + 16) + 16
     pad = {1: 1, 2: 2, 3: 1, 4: 4, 5: 2, 6: 4}[variant]

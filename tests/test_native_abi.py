@@ -44,6 +44,6 @@ def test_program_stride_is_host_callable():
     s32 = _native.lib().an_program_stride(128, 512, 8, 0)
     s64 = _native.lib().an_program_stride(128, 512, 8, 1)
     assert s32 % 16 == 0 and s64 > s32
-    # header 32 + out slots 16 + groups 16N + steps 16N + u16 src / f32 w x (3C+8N+16)
-    e = 3 * 512 + 8 * 128 + 16
+    # header 32 + out slots 16 + groups 16N + steps 16N + u16 src / f32 w x (3C+12N+16)
+    e = 3 * 512 + 12 * 128 + 16
     assert s32 == 32 + 16 + 128 * 16 + 128 * 16 + 2 * e + 4 * e

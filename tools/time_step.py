@@ -1,0 +1,38 @@
+"""Wall/CUDA-event breakdown of one bench step (transform, finalize, plan, forward)."""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2404_01817_b200 as tn  # noqa: E402
+from paper_2404_01817_b200.synthetic import synthetic_population  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--pop", type=int, default=10000)
+ap.add_argument("--variant", type=int, default=0)
+ap.add_argument("--reps", type=int, default=4)
+a = ap.parse_args()
+n, c = synthetic_population(a.pop, 128, 512, 32, 8, seed=20261018)
+nodes, conns = torch.from_numpy(n).cuda(), torch.from_numpy(c).cuda()
+x = torch.randn((a.pop, 4096, 32), device="cuda")
+out = torch.empty((a.pop, 4096, 8), device="cuda")
+for rep in range(a.reps):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8, sync=False)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    tn.finalize_transform(st)
+    t2 = time.perf_counter()
+    v = (a.variant & 0xF) or 5
+    plan = tn.inference._bucket_plan(st, v)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    tn.forward_device(st, x, out, variant=a.variant)
+    torch.cuda.synchronize()
+    t4 = time.perf_counter()
+    print(f"transform {1e3*(t1-t0):.2f} ms finalize {1e3*(t2-t1):.2f} plan {1e3*(t3-t2):.2f} "
+          f"forward {1e3*(t4-t3):.2f} buckets {len(plan)} maxdims {st.maxdims}", flush=True)
