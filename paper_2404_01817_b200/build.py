@@ -57,7 +57,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
         src, obj = pair
         if not force and not _stale(obj, src):
             return obj, ""
-        cmd = [nvcc, *ARCH, *FLAGS, *PER_FILE.get(os.path.basename(src), []), "-I", CSRC, "-c", src, "-o", obj]
+        extra = os.environ.get("TNEAT_NVCC_EXTRA", "").split()  # tuning experiments (-D knobs) only
+        cmd = [nvcc, *ARCH, *FLAGS, *PER_FILE.get(os.path.basename(src), []), *extra, "-I", CSRC, "-c", src,
+               "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         res = subprocess.run(cmd, capture_output=True, text=True)

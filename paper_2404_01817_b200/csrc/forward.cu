@@ -31,6 +31,11 @@ namespace tneat {
 
 template <typename T, int S> struct __align__(sizeof(T) * S) Pack { T v[S]; };
 
+// TMA-engine prefetch of a contiguous block into L2 (bytes: multiple of 16)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // finish one step: aggregate -> bias + response * agg -> activation -> slot
 template <int S, int RB>
 __device__ __forceinline__ void finish_step(const StepT<float>& st, const float (&acc)[S], char* vb) {
@@ -96,31 +101,50 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint16_t
                                               const float* __restrict__ w_s,
                                               const StepT<float>* __restrict__ st, char* vb) {
   constexpr int GW = G == 3 ? 4 : G;
+  constexpr int SP = (S + 1) / 2;  // sample pairs: Blackwell packed fp32 (FFMA2 / FADD2)
   using PackT = Pack<float, S>;
-  float acc[G][S];
+  float2 acc[G][SP];
 #pragma unroll
   for (int j = 0; j < G; ++j)
 #pragma unroll
-    for (int s = 0; s < S; ++s) acc[j][s] = 0.0f;
+    for (int p = 0; p < SP; ++p) acc[j][p] = make_float2(0.0f, 0.0f);
   const uint16_t* sp = src_s + gr.e_begin;
   const float* wp = w_s + gr.e_begin;
   const int rounds = gr.rounds;  // even; holes read the zero slot with weight 0
+  // program words of the next two rounds are loaded while this pair's values
+  // are in flight (the block is followed by more program / value memory, so
+  // the look-ahead past the last round stays inside shared memory)
+  uint32_t sl[2 * GW];
+  float w[2 * GW];
+  if (rounds > 0) {
+    load_u16<2 * GW>(sp, sl);
+    load_f32<2 * GW>(wp, w);
+  }
 #pragma unroll 1
   for (int r = 0; r < rounds; r += 2) {
-    uint32_t sl[2 * GW];
-    float w[2 * GW];
-    load_u16<2 * GW>(sp + r * GW, sl);
-    load_f32<2 * GW>(wp + r * GW, w);
     PackT v[2 * GW];
 #pragma unroll
     for (int q = 0; q < 2 * GW; ++q)
       if (q % GW < G) v[q] = *reinterpret_cast<const PackT*>(vb + sl[q] * RB);
+    float wc[2 * GW];
+#pragma unroll
+    for (int q = 0; q < 2 * GW; ++q) wc[q] = w[q];
+    load_u16<2 * GW>(sp + (r + 2) * GW, sl);
+    load_f32<2 * GW>(wp + (r + 2) * GW, w);
+#define w wc
 #pragma unroll
     for (int q = 0; q < 2 * GW; ++q)
       if (q % GW < G) {
+        if constexpr (S == 1) {
+          acc[q % GW][0].x = fmaf(w[q], v[q].v[0], acc[q % GW][0].x);
+        } else {
 #pragma unroll
-        for (int s = 0; s < S; ++s) acc[q % GW][s] = fmaf(w[q], v[q].v[s], acc[q % GW][s]);
+          for (int p = 0; p < SP; ++p)  // one FFMA2 per edge and sample pair (exact fp32 FMA per lane)
+            acc[q % GW][p] = __ffma2_rn(make_float2(w[q], w[q]), make_float2(v[q].v[2 * p], v[q].v[2 * p + 1]),
+                                        acc[q % GW][p]);
+        }
       }
+#undef w
   }
   if constexpr (TANH) {
     // tanh(b + r*a) = 2 / (1 + 2^(k (b + r*a))) - 1, k = -2 log2(e): one FFMA into
@@ -131,14 +155,29 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint16_t
       const StepT<float> sj = st[j];
       const float rk = sj.resp * K, bk = sj.bias * K;
       PackT y;
+      if constexpr (S == 1) {
+        y.v[0] = fmaf(2.0f, rcp_approx(1.0f + ex2_approx(fmaf(rk, acc[j][0].x, bk))), -1.0f);
+      } else {
 #pragma unroll
-      for (int s = 0; s < S; ++s)
-        y.v[s] = fmaf(2.0f, rcp_approx(1.0f + ex2_approx(fmaf(rk, acc[j][s], bk))), -1.0f);
+        for (int p = 0; p < SP; ++p) {
+          const float2 t = __ffma2_rn(make_float2(rk, rk), acc[j][p], make_float2(bk, bk));
+          const float2 d = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(ex2_approx(t.x), ex2_approx(t.y)));
+          const float2 yy = __ffma2_rn(make_float2(2.0f, 2.0f), make_float2(rcp_approx(d.x), rcp_approx(d.y)),
+                                       make_float2(-1.0f, -1.0f));
+          y.v[2 * p] = yy.x;
+          y.v[2 * p + 1] = yy.y;
+        }
+      }
       if (sj.slot != NO_SLOT) *reinterpret_cast<PackT*>(vb + sj.slot * RB) = y;
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < G; ++j) finish_step<S, RB>(st[j], acc[j], vb);
+    for (int j = 0; j < G; ++j) {
+      float a[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) a[s] = (s & 1) ? acc[j][s / 2].y : acc[j][s / 2].x;
+      finish_step<S, RB>(st[j], a, vb);
+    }
   }
 }
 
@@ -228,10 +267,17 @@ __device__ __forceinline__ void run_group(const GroupRec& gr, const uint16_t* sr
   }
 }
 
+// register cap: at least TNEAT_TILE_WARPS resident warps per SM (shared memory
+// permitting), i.e. <= 64K / (32 * warps) registers per thread
+#ifndef TNEAT_TILE_WARPS
+#define TNEAT_TILE_WARPS 16
+#endif
+#define TNEAT_TILE_MINB(nt) (TNEAT_TILE_WARPS * 32 / (nt) > 0 ? TNEAT_TILE_WARPS * 32 / (nt) : 1)
+
 // grid: one CTA per (genome, run of `tpc` consecutive tiles); the genome's
 // program is staged in shared memory once and reused for every tile
 template <typename T, int S, int NT>
-__global__ void __launch_bounds__(NT, 1) fwd_tile_kernel(const uint8_t* __restrict__ prog, ProgLayout L,
+__global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const uint8_t* __restrict__ prog, ProgLayout L,
                                                       const int32_t* __restrict__ genome_ids,
                                                       const T* __restrict__ in, int64_t in_gstride,
                                                       int B, int I, int O, int runs, int tpc,
@@ -260,6 +306,10 @@ __global__ void __launch_bounds__(NT, 1) fwd_tile_kernel(const uint8_t* __restri
   float* w_s = reinterpret_cast<float*>(smem + off_w);
   EdgeD* ed_s = reinterpret_cast<EdgeD*>(smem + off_w);
   T* vals = reinterpret_cast<T*>(smem + align_up(off_w + w_bytes, 16));
+  if (sizeof(T) == 4 && tid == 0 && (((uintptr_t)in | (uint32_t)(I * 4) | (uint64_t)in_gstride * 4) & 15) == 0) {
+    const int t0 = run * tpc * TT;  // first tile of this CTA: in flight while the program is staged
+    if (t0 < B) prefetch_l2(in + gi * in_gstride + (int64_t)t0 * I, (uint32_t)(min(TT, B - t0) * I * 4));
+  }
   {
     auto copy16 = [&](void* dst, const void* src, int64_t bytes) {
       const int n16 = (int)(bytes / 16);
@@ -283,13 +333,9 @@ __global__ void __launch_bounds__(NT, 1) fwd_tile_kernel(const uint8_t* __restri
   const T* gin = in + gi * in_gstride;
   T* go = out + gi * out_gstride;
   char* vb = reinterpret_cast<char*>(vals) + tid * S * sizeof(T);
-  uint32_t osl[8];
   bool fast_out = sizeof(T) == 4 && O == 8;
 #pragma unroll
-  for (int o = 0; o < 8; ++o) {
-    osl[o] = oslot[o];
-    fast_out = fast_out && osl[o] != NO_SLOT;
-  }
+  for (int o = 0; o < 8; ++o) fast_out = fast_out && oslot[o] != NO_SLOT;
   const int tile_end = min((run + 1) * tpc, (B + TT - 1) / TT);
   const bool vec_in = sizeof(T) == 4 && (I & 3) == 0 && (in_gstride & 3) == 0;
   const int step_s = (4 * NT) / I, step_i = (4 * NT) - step_s * I;  // chunk stride in (sample, input)
@@ -301,21 +347,9 @@ __global__ void __launch_bounds__(NT, 1) fwd_tile_kernel(const uint8_t* __restri
   // (samples x I) block is contiguous in HBM: it is read with coalesced 16-byte
   // loads and scattered into the [slot][sample] layout (rows padded by S
   // elements, so a warp's scattered stores hit distinct banks).  The next
-  // tile's chunks are prefetched into registers while this tile computes, so
-  // the HBM latency is off the critical path.
-  constexpr int PFMAX = 4 * S;  // register prefetch only when S * I / 4 <= 4 * S (I <= 16)
-  const bool prefetch = vec_in && S * I / 4 <= PFMAX;
-  const int per_thread = S * I / 4;
-  float4 pf[PFMAX];
-#define TNEAT_ISSUE(tile_)                                                                \
-  {                                                                                       \
-    const int t0_ = (tile_) * TT, n4_ = min(TT, B - t0_) * I / 4;                         \
-    const float4* src_ = reinterpret_cast<const float4*>(gin + (int64_t)t0_ * I);         \
-    _Pragma("unroll") for (int k = 0; k < PFMAX; ++k) {                                   \
-      const int c = tid + k * NT;                                                         \
-      if (k < per_thread && c < n4_) pf[k] = __ldg(src_ + c);                             \
-    }                                                                                     \
-  }
+  // tile's block is prefetched into L2 by the TMA engine while this tile
+  // computes, so the tile-start loads are L2 hits.
+  const bool pf_l2 = sizeof(T) == 4 && (((uintptr_t)gin | (uint32_t)(I * 4)) & 15) == 0;
   float* const vf = reinterpret_cast<float*>(vals);
 #define TNEAT_SCATTER4(sm_, i_, x_)                 \
   {                                                 \
@@ -325,31 +359,21 @@ __global__ void __launch_bounds__(NT, 1) fwd_tile_kernel(const uint8_t* __restri
     base_[2 * (RB / 4)] = (x_).z;                   \
     base_[3 * (RB / 4)] = (x_).w;                   \
   }
-  if (prefetch) TNEAT_ISSUE(run * tpc);
   for (int tile = run * tpc; tile < tile_end; ++tile) {
     const int t0 = tile * TT;
     const int nt = min(TT, B - t0);
     if (tile != run * tpc) __syncthreads();  // previous tile fully consumed
-    if (prefetch) {
+    if (pf_l2 && tid == 0 && tile + 1 < tile_end) {
+      const int t1 = t0 + TT;
+      prefetch_l2(gin + (int64_t)t1 * I, (uint32_t)(min(TT, B - t1) * I * 4));
+    }
+    if (vec_in && cps_shift >= 0) {  // I/4 chunks per input row is a power of two
+      const float4* src = reinterpret_cast<const float4*>(gin + (int64_t)t0 * I);
       const int n4 = nt * I / 4;
-      if (cps_shift >= 0) {  // I/4 chunks per input row is a power of two
-#pragma unroll
-        for (int k = 0; k < PFMAX; ++k) {
-          const int c = tid + k * NT;
-          if (k < per_thread && c < n4) TNEAT_SCATTER4(c >> cps_shift, (c & cps_mask) << 2, pf[k]);
-        }
-      } else {
-        int sm = (4 * tid) / I, i = 4 * tid - sm * I;
-#pragma unroll
-        for (int k = 0; k < PFMAX; ++k) {
-          const int c = tid + k * NT;
-          if (k < per_thread && c < n4) TNEAT_SCATTER4(sm, i, pf[k]);
-          i += step_i;
-          sm += step_s;
-          if (i >= I) { i -= I; ++sm; }
-        }
+      for (int c = tid; c < n4; c += NT) {
+        const float4 x = __ldg(src + c);
+        TNEAT_SCATTER4(c >> cps_shift, (c & cps_mask) << 2, x);
       }
-      if (tile + 1 < tile_end) TNEAT_ISSUE(tile + 1);
     } else if (vec_in) {
       const float4* src = reinterpret_cast<const float4*>(gin + (int64_t)t0 * I);
       const int n4 = nt * I / 4;
@@ -395,7 +419,7 @@ __global__ void __launch_bounds__(NT, 1) fwd_tile_kernel(const uint8_t* __restri
     if (fast_out) {
       PackT v[8];
 #pragma unroll
-      for (int o = 0; o < 8; ++o) v[o] = *reinterpret_cast<const PackT*>(vb + osl[o] * RB);
+      for (int o = 0; o < 8; ++o) v[o] = *reinterpret_cast<const PackT*>(vb + (uint32_t)oslot[o] * RB);
 #pragma unroll
       for (int j = 0; j < S; ++j) {
         if (s0 + j >= B) break;
