@@ -91,13 +91,60 @@ __device__ __forceinline__ void load_f32(const float* p, float (&out)[N]) {
   }
 }
 
+template <int N>
+__device__ __forceinline__ void load_u32(const uint32_t* p, uint32_t (&out)[N]) {
+  if constexpr (N == 2) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    out[0] = v.x; out[1] = v.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < N / 4; ++i) {
+      const uint4 v = reinterpret_cast<const uint4*>(p)[i];
+      out[4 * i] = v.x; out[4 * i + 1] = v.y; out[4 * i + 2] = v.z; out[4 * i + 3] = v.w;
+    }
+  }
+}
+
+// two rounds of a sum group: 2*GW value loads (byte offsets into the thread's
+// value column), then one FFMA2 (or FFMA for S = 1) per edge and sample pair
+template <int S, int G, int GW>
+__device__ __forceinline__ void sum_rounds(float2 (&acc)[G][(S + 1) / 2], const uint32_t (&off)[2 * GW],
+                                           const float (&w)[2 * GW], const char* vb) {
+  using PackT = Pack<float, S>;
+  PackT v[2 * GW];
+#pragma unroll
+  for (int q = 0; q < 2 * GW; ++q)
+    if (q % GW < G) {
+#ifdef TNEAT_DIAG_NOLDS  // diagnostic builds only: value loads replaced by the offset
+      for (int s = 0; s < S; ++s) v[q].v[s] = __uint_as_float(off[q]);
+#else
+      v[q] = *reinterpret_cast<const PackT*>(vb + off[q]);
+#endif
+    }
+#pragma unroll
+  for (int q = 0; q < 2 * GW; ++q)
+    if (q % GW < G) {
+      if constexpr (S == 1) {
+        acc[q % GW][0].x = fmaf(w[q], v[q].v[0], acc[q % GW][0].x);
+      } else {
+#pragma unroll
+        for (int p = 0; p < S / 2; ++p)  // one FFMA2 per edge and sample pair (exact fp32 FMA per lane)
+          acc[q % GW][p] = __ffma2_rn(make_float2(w[q], w[q]), make_float2(v[q].v[2 * p], v[q].v[2 * p + 1]),
+                                      acc[q % GW][p]);
+      }
+    }
+}
+
 // One sum/mean group of G steps (fp32 program): edge block of width GW = G|4,
-// two rounds per iteration (2*GW sources in one <=16-byte load, weights in
-// <=2 16-byte loads) and up to 2G independent value loads / FMA chains.
-// All rounds run unpredicated (holes are zero-slot entries).  TANH: every
-// step is tanh/sum (short epilogue).
+// two rounds per step of the pipeline (2*GW byte offsets in <= two 16-byte
+// loads, weights likewise) and up to 2G independent value loads / FMA chains,
+// all unpredicated (holes are zero-slot entries).  Program words are
+// double-buffered: the next two rounds' words load while this pair's values
+// are in flight (the look-ahead past the block's end stays inside shared
+// memory: weights and value slots follow the offsets).  TANH: every step is
+// tanh/sum (short epilogue).
 template <int S, int G, int RB, bool TANH>
-__device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint16_t* __restrict__ src_s,
+__device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t* __restrict__ off_s,
                                               const float* __restrict__ w_s,
                                               const StepT<float>* __restrict__ st, char* vb) {
   constexpr int GW = G == 3 ? 4 : G;
@@ -108,43 +155,24 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint16_t
   for (int j = 0; j < G; ++j)
 #pragma unroll
     for (int p = 0; p < SP; ++p) acc[j][p] = make_float2(0.0f, 0.0f);
-  const uint16_t* sp = src_s + gr.e_begin;
+  const uint32_t* op = off_s + gr.e_begin;
   const float* wp = w_s + gr.e_begin;
   const int rounds = gr.rounds;  // even; holes read the zero slot with weight 0
-  // program words of the next two rounds are loaded while this pair's values
-  // are in flight (the block is followed by more program / value memory, so
-  // the look-ahead past the last round stays inside shared memory)
-  uint32_t sl[2 * GW];
-  float w[2 * GW];
+  uint32_t oa[2 * GW], ob[2 * GW];
+  float wa[2 * GW], wb[2 * GW];
   if (rounds > 0) {
-    load_u16<2 * GW>(sp, sl);
-    load_f32<2 * GW>(wp, w);
+    load_u32<2 * GW>(op, oa);
+    load_f32<2 * GW>(wp, wa);
   }
 #pragma unroll 1
-  for (int r = 0; r < rounds; r += 2) {
-    PackT v[2 * GW];
-#pragma unroll
-    for (int q = 0; q < 2 * GW; ++q)
-      if (q % GW < G) v[q] = *reinterpret_cast<const PackT*>(vb + sl[q] * RB);
-    float wc[2 * GW];
-#pragma unroll
-    for (int q = 0; q < 2 * GW; ++q) wc[q] = w[q];
-    load_u16<2 * GW>(sp + (r + 2) * GW, sl);
-    load_f32<2 * GW>(wp + (r + 2) * GW, w);
-#define w wc
-#pragma unroll
-    for (int q = 0; q < 2 * GW; ++q)
-      if (q % GW < G) {
-        if constexpr (S == 1) {
-          acc[q % GW][0].x = fmaf(w[q], v[q].v[0], acc[q % GW][0].x);
-        } else {
-#pragma unroll
-          for (int p = 0; p < SP; ++p)  // one FFMA2 per edge and sample pair (exact fp32 FMA per lane)
-            acc[q % GW][p] = __ffma2_rn(make_float2(w[q], w[q]), make_float2(v[q].v[2 * p], v[q].v[2 * p + 1]),
-                                        acc[q % GW][p]);
-        }
-      }
-#undef w
+  for (int r = 0; r < rounds; r += 4) {
+    load_u32<2 * GW>(op + (r + 2) * GW, ob);
+    load_f32<2 * GW>(wp + (r + 2) * GW, wb);
+    sum_rounds<S, G, GW>(acc, oa, wa, vb);
+    if (r + 2 >= rounds) break;
+    load_u32<2 * GW>(op + (r + 4) * GW, oa);
+    load_f32<2 * GW>(wp + (r + 4) * GW, wa);
+    sum_rounds<S, G, GW>(acc, ob, wb, vb);
   }
   if constexpr (TANH) {
     // tanh(b + r*a) = 2 / (1 + 2^(k (b + r*a))) - 1, k = -2 log2(e): one FFMA into
@@ -161,9 +189,13 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint16_t
 #pragma unroll
         for (int p = 0; p < SP; ++p) {
           const float2 t = __ffma2_rn(make_float2(rk, rk), acc[j][p], make_float2(bk, bk));
+#ifdef TNEAT_DIAG_NOACT  // diagnostic builds only: no MUFU in the epilogue
+          const float2 yy = t;
+#else
           const float2 d = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(ex2_approx(t.x), ex2_approx(t.y)));
           const float2 yy = __ffma2_rn(make_float2(2.0f, 2.0f), make_float2(rcp_approx(d.x), rcp_approx(d.y)),
                                        make_float2(-1.0f, -1.0f));
+#endif
           y.v[2 * p] = yy.x;
           y.v[2 * p + 1] = yy.y;
         }
@@ -209,7 +241,7 @@ __device__ __forceinline__ void run_sum_group_f64(const GroupRec& gr, const Edge
 
 // singleton group with a non-sum aggregation (product / max / min), exact count
 template <typename T, int S, int RB>
-__device__ __forceinline__ void run_generic_step(const GroupRec& gr, const uint16_t* __restrict__ src_s,
+__device__ __forceinline__ void run_generic_step(const GroupRec& gr, const uint32_t* __restrict__ off_s,
                                                  const float* __restrict__ w_s, const EdgeD* __restrict__ ed_s,
                                                  const StepT<T>& st, char* vb) {
   T acc[S];
@@ -217,11 +249,11 @@ __device__ __forceinline__ void run_generic_step(const GroupRec& gr, const uint1
 #pragma unroll
   for (int s = 0; s < S; ++s) acc[s] = neutral;
   for (int e = 0; e < st.count; ++e) {
-    uint32_t src;
+    uint32_t off;  // byte offset of the source slot in the thread's value column
     T w;
-    if constexpr (sizeof(T) == 8) { src = ed_s[gr.e_begin + e].src; w = ed_s[gr.e_begin + e].w; }
-    else { src = src_s[gr.e_begin + e]; w = w_s[gr.e_begin + e]; }
-    const Pack<T, S> v = *reinterpret_cast<const Pack<T, S>*>(vb + src * RB);
+    if constexpr (sizeof(T) == 8) { off = ed_s[gr.e_begin + e].src * RB; w = ed_s[gr.e_begin + e].w; }
+    else { off = off_s[gr.e_begin + e]; w = w_s[gr.e_begin + e]; }
+    const Pack<T, S> v = *reinterpret_cast<const Pack<T, S>*>(vb + off);
 #pragma unroll
     for (int s = 0; s < S; ++s) acc[s] = agg_combine<T>(st.agg, acc[s], w * v.v[s]);
   }
@@ -235,7 +267,7 @@ __device__ __forceinline__ void run_generic_step(const GroupRec& gr, const uint1
 }
 
 template <typename T, int S, int RB>
-__device__ __forceinline__ void run_group(const GroupRec& gr, const uint16_t* src_s, const float* w_s,
+__device__ __forceinline__ void run_group(const GroupRec& gr, const uint32_t* src_s, const float* w_s,
                                           const EdgeD* ed_s, const StepT<T>* st, char* vb) {
   if (!(gr.cls & GRP_GENERIC)) {
     if constexpr (sizeof(T) == 4) {
@@ -299,10 +331,11 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
   const int64_t off_st = (int64_t)n_groups * sizeof(GroupRec);
   StepT<T>* st_s = reinterpret_cast<StepT<T>*>(smem + off_st);
   const int64_t off_src = off_st + (int64_t)n_steps * sizeof(StepT<T>);
-  const int64_t src_bytes = sizeof(T) == 8 ? 0 : align_up(2ll * n_edges, 16);
+  // fp32: u16 source slots are expanded to u32 byte offsets (slot * RB) in shared memory
+  const int64_t src_bytes = sizeof(T) == 8 ? 0 : align_up(4ll * n_edges, 16);
   const int64_t off_w = off_src + src_bytes;
   const int64_t w_bytes = sizeof(T) == 8 ? 16ll * n_edges : 4ll * n_edges;
-  uint16_t* src_s = reinterpret_cast<uint16_t*>(smem + off_src);
+  uint32_t* src_s = reinterpret_cast<uint32_t*>(smem + off_src);
   float* w_s = reinterpret_cast<float*>(smem + off_w);
   EdgeD* ed_s = reinterpret_cast<EdgeD*>(smem + off_w);
   T* vals = reinterpret_cast<T*>(smem + align_up(off_w + w_bytes, 16));
@@ -318,7 +351,13 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
     };
     copy16(gr_s, gp + L.off_groups, off_st);
     copy16(st_s, gp + L.off_steps, (int64_t)n_steps * sizeof(StepT<T>));
-    if (sizeof(T) == 4) copy16(src_s, gp + L.off_src, src_bytes);
+    if (sizeof(T) == 4) {
+      const uint32_t* gs = reinterpret_cast<const uint32_t*>(gp + L.off_src);  // u16 pairs
+      for (int i = tid; i < n_edges / 2; i += NT) {
+        const uint32_t pr = __ldg(gs + i);
+        reinterpret_cast<uint2*>(src_s)[i] = make_uint2((pr & 0xFFFFu) * RB, (pr >> 16) * RB);
+      }
+    }
     copy16(reinterpret_cast<void*>(smem + off_w), gp + L.off_w, w_bytes);
   }
   // output slots of this genome (first 8 staged in shared memory)
@@ -671,7 +710,7 @@ int launch_tile(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, co
   if (grid > 0x7FFFFFFFll) return -5;
   const int64_t ms = maxdims_host[1], me = maxdims_host[2];
   const int64_t prog_bytes = ms * sizeof(GroupRec) + ms * sizeof(StepT<T>) +
-                             (sizeof(T) == 8 ? 16 * me : align_up(2 * me, 16) + 4 * me);
+                             (sizeof(T) == 8 ? 16 * me : align_up(4 * me, 16) + 4 * me);
   int64_t smem = align_up(prog_bytes, 16) + (int64_t)max(maxdims_host[0], I) * (TT + S) * sizeof(T);
   if (const char* pad = getenv("TNEAT_EXPERIMENT_SMEM_PAD")) smem += atoll(pad);  // occupancy experiments only
   if (smem > 227 * 1024) return -6;

@@ -19,6 +19,12 @@
 namespace tneat {
 
 constexpr uint64_t U64_MAX = ~0ull;
+// group join rule: a step joins if DEN * count >= NUM * (longest count); 1/2
+// bounds the padded entries (edge_capacity) -- tighter rules only shrink them
+#ifndef TNEAT_JOIN_NUM
+#define TNEAT_JOIN_NUM 1
+#define TNEAT_JOIN_DEN 2
+#endif
 constexpr int32_t NEVER = 0x7FFFFFFF;
 constexpr uint8_t F_LIVE = 1, F_INPUT = 2, F_OUTPUT = 4, F_FREED = 8;
 
@@ -63,14 +69,19 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, Warp
     o += bytes;
     return at;
   };
-  const int64_t a_skey = take(8ll * Npad, 8), a_ekey = take(8ll * Cpad, 8), a_gkey = take(8ll * Npad, 8);
-  const int64_t a_ekey2 = take(8ll * (C > 0 ? C : 1), 8);
+  const int64_t a_skey = take(8ll * Npad, 8), a_ekey = take(8ll * Cpad, 8);
+  // union: ekey2 (edge staging, dead once the CSR is built) shares memory with
+  // the arrays that are first written after Kahn (gkey, grp, last_grp,
+  // step_row, grp_of)
+  const int64_t a_union = take(0, 16);
+  const int64_t a_gkey = take(8ll * Npad, 8), a_grp = take(16ll * N, 16), a_last = take(4ll * N, 4);
+  const int64_t a_srow = take(2ll * N, 2), a_grpof = take(2ll * N, 2);
+  const int64_t a_ekey2 = a_union;
+  o = a_union + (o - a_union > 8ll * (C > 0 ? C : 1) ? o - a_union : 8ll * (C > 0 ? C : 1));
   const int64_t a_indeg = take(4ll * N, 4), a_outdeg = take(4ll * N, 4);
   const int64_t a_in = take(4ll * (N + 1), 4), a_su = take(4ll * (N + 1), 4);
-  const int64_t a_lvl = take(4ll * N, 4), a_last = take(4ll * N, 4);
-  const int64_t a_grp = take(16ll * N, 16);
+  const int64_t a_lvl = take(4ll * N, 4);
   const int64_t a_succ = take(2ll * C, 2), a_order = take(2ll * N, 2), a_slot = take(2ll * N, 2);
-  const int64_t a_srow = take(2ll * N, 2), a_grpof = take(2ll * N, 2);
   const int64_t a_flags = take(N, 1), a_needed = take(N, 1), a_used = take(N, 1);
   const int64_t a_ready = take(4ll * W, 4), a_free = take(4ll * WS, 4);
   if (kCarve) {
@@ -399,7 +410,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       const int cls = (int)((key >> 47) & 1);
       const int lv = (int)(key >> 48);
       const bool join = ng > 0 && lv == cur_lv && cls == cur_cls && cls == 0 && s.grp[ng - 1].n < 4 &&
-                        2 * cnt >= cur_rounds;
+                        TNEAT_JOIN_DEN * cnt >= TNEAT_JOIN_NUM * cur_rounds;
       if (!join) {
         if (ng > 0) e_total = (int)align_up(e_total + group_width(s.grp[ng - 1].n) * s.grp[ng - 1].rounds, 8);
         GroupRec gr;

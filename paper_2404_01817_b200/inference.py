@@ -296,11 +296,12 @@ def _bucket_plan(stacked: StackedNetworks, variant: int) -> list:
     slots = stacked._cache.get("slots")
     if slots is None:
         slots = stacked.program[:, 8:12].contiguous().view(torch.int32).reshape(-1).cpu().numpy()
-    order = np.argsort(slots, kind="stable").astype(np.int32)
+    # slot counts are small integers: a 16-bit key makes numpy's stable sort a radix sort
+    order = np.argsort(np.minimum(slots, 65535).astype(np.uint16), kind="stable").astype(np.int32)
     sorted_slots = slots[order]
     ids = torch.from_numpy(order).to(stacked.program.device)  # 4P bytes; no pinned allocation per plan
     _, ms, me = stacked.maxdims
-    prog = 32 * ms + (16 * me if stacked.precision else 6 * me + 16) + 16
+    prog = 32 * ms + (16 * me if stacked.precision else 8 * me + 16) + 16
     pad = {1: 1, 2: 2, 3: 1, 4: 4, 5: 2, 6: 4}[variant]
     occ = _SMEM_PER_SM // (prog + np.maximum(sorted_slots, stacked.num_inputs) * (tt + pad) * esz + 1024)
     plan = []
