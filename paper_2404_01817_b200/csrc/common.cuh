@@ -86,21 +86,25 @@ template <> struct __align__(16) StepT<double> {
 // arrays, u16 source slots and f32 weights (6 bytes per edge)
 struct __align__(16) EdgeD { uint32_t src; uint32_t pad; double w; };
 
-// Split layout (format bit FMT_SPLIT, fp32 only): the inputs live in TMEM
-// columns (column = input key) and only hidden values take shared-memory slots;
-// each group keeps two interleaved edge blocks -- input-sourced edges (sources
-// are TMEM columns) and hidden-sourced edges (sources are hidden slots).
+// Split programs (format bit FMT_SPLIT, fp32 feed-forward; forward.cu
+// fwd_split_kernel): input values live in tensor memory, hidden values in
+// shared-memory slots numbered from 0 (inputs take no slot).  Each group has
+// two interleaved edge blocks with the GroupRec layout: the input block
+// (source = input key, a TMEM column group; holes read input 0 with weight
+// 0) and the hidden block (source = hidden slot; holes read the zero slot).
+// Sum/mean groups pad both blocks to even rounds; non-sum steps are
+// singletons with exact counts in both blocks.
 struct __align__(16) GroupSplit {  // 32 bytes
   uint8_t n;
   uint8_t cls;
-  uint16_t rounds_in;
-  uint16_t rounds_h;
   uint16_t step_begin;
-  uint16_t e_in;       // first entry of the input-edge block (multiple of 8)
-  uint16_t e_h;        // first entry of the hidden-edge block (multiple of 8)
+  uint16_t rounds_in;  // input block rounds
+  uint16_t e_in;       // first input-block entry (multiple of 8)
+  uint16_t rounds_h;   // hidden block rounds
+  uint16_t e_h;        // first hidden-block entry (multiple of 8)
   uint16_t pad[2];
-  uint16_t cnt_in[4];
-  uint16_t cnt_h[4];
+  uint16_t cnt_in[4];  // input edges of each step
+  uint16_t cnt_h[4];   // hidden edges of each step
 };
 
 enum : int { FMT_F64 = 1, FMT_SPLIT = 2 };
@@ -118,8 +122,9 @@ __host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + 
 // <= 8/3 x real), rounds are even (+gw <= 4 per group) and every group starts
 // on a multiple of 8 (+7)
 __host__ __device__ inline int64_t edge_capacity(int N, int C) { return 3ll * C + 12ll * N + 16; }
-// split layout: two padded blocks per group (each <= 2x its real entries) + alignment
-__host__ __device__ inline int64_t edge_capacity_split(int N, int C) { return 4ll * C + 16ll * N + 16; }
+// split programs: input blocks obey the bound above; a hidden block is padded
+// to its longest list (<= 4x real); both blocks round and align per group
+__host__ __device__ inline int64_t edge_capacity_split(int N, int C) { return 7ll * C + 24ll * N + 16; }
 
 struct ProgLayout {
   int64_t off_out, off_groups, off_steps, off_src, off_w, stride;

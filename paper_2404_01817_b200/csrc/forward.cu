@@ -26,6 +26,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace tneat {
 
@@ -482,6 +483,365 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
 }
 
 // ---------------------------------------------------------------------------
+// split-program forward: input values in tensor memory, hidden values in
+// shared memory
+// ---------------------------------------------------------------------------
+//
+// One CTA of 128 threads (4 warps; warp w owns TMEM lanes 32w..32w+31) per
+// (genome, run of `tpc` tiles of 128*S inputs).  Thread t owns samples
+// t*S..t*S+S-1: it loads its own input rows (16-byte loads, L2-prefetched by the
+// TMA engine), stores them to its TMEM lane (column k*S + s = input k of sample
+// s; tcgen05.st) and reads them back per input edge with one tcgen05.ld of S
+// columns.  Only the hidden values occupy shared memory ([slot][128*S + S]),
+// so a CTA needs roughly a third of the tile kernel's shared memory per input
+// and more warps stay resident.  Every value a thread reads it wrote itself
+// (TMEM lane / shared column), so the tile loop has no CTA barrier.
+// Input-block holes read input 0 with weight 0; a tile whose inputs are not all
+// finite runs the exact variant that skips holes (inf * 0 would be NaN).
+#ifndef TNEAT_SPLIT_WARPS
+#define TNEAT_SPLIT_WARPS 24
+#endif
+constexpr int SPLIT_NT = 128;
+
+__device__ __forceinline__ GroupSplit decode_group(const GroupSplit* gs, int g) {
+  const uint4 a = reinterpret_cast<const uint4*>(gs)[2 * g];
+  const uint4 b = reinterpret_cast<const uint4*>(gs)[2 * g + 1];
+  GroupSplit gr;
+  gr.n = (uint8_t)(a.x & 0xFF);
+  gr.cls = (uint8_t)((a.x >> 8) & 0xFF);
+  gr.step_begin = (uint16_t)(a.x >> 16);
+  gr.rounds_in = (uint16_t)(a.y & 0xFFFF);
+  gr.e_in = (uint16_t)(a.y >> 16);
+  gr.rounds_h = (uint16_t)(a.z & 0xFFFF);
+  gr.e_h = (uint16_t)(a.z >> 16);
+  gr.cnt_in[0] = (uint16_t)(b.x & 0xFFFF);
+  gr.cnt_in[1] = (uint16_t)(b.x >> 16);
+  gr.cnt_in[2] = (uint16_t)(b.y & 0xFFFF);
+  gr.cnt_in[3] = (uint16_t)(b.y >> 16);
+  gr.cnt_h[0] = (uint16_t)(b.z & 0xFFFF);
+  gr.cnt_h[1] = (uint16_t)(b.z >> 16);
+  gr.cnt_h[2] = (uint16_t)(b.w & 0xFFFF);
+  gr.cnt_h[3] = (uint16_t)(b.w >> 16);
+  return gr;
+}
+
+// input-block helpers: issue the TMEM loads of two rounds (up to 2*GW loads of
+// S columns; holes load input 0), and the FMAs once they have landed.
+// EXACT: entries past a step's count are skipped (non-finite inputs).
+template <int S, int G, int GW>
+__device__ __forceinline__ void input_issue(float (&v)[2 * GW * S], const uint32_t (&col)[2 * GW], uint32_t tlane,
+                                            uint32_t cmask) {
+#pragma unroll
+  for (int q = 0; q < 2 * GW; ++q)
+    if (q % GW < G) tmem_ld_cols<S>(tlane + (col[q] & cmask), v + q * S);
+}
+template <int S, int G, int GW, bool EXACT>
+__device__ __forceinline__ void input_fma(float2 (&acc)[G][(S + 1) / 2], const float (&v)[2 * GW * S],
+                                          const float (&w)[2 * GW], int r, const uint16_t (&cnt)[4]) {
+#pragma unroll
+  for (int q = 0; q < 2 * GW; ++q)
+    if (q % GW < G && (!EXACT || r + q / GW < cnt[q % GW])) {
+      if constexpr (S == 1) {
+        acc[q % GW][0].x = fmaf(w[q], v[q], acc[q % GW][0].x);
+      } else {
+#pragma unroll
+        for (int p = 0; p < S / 2; ++p)
+          acc[q % GW][p] = __ffma2_rn(make_float2(w[q], w[q]), make_float2(v[q * S + 2 * p], v[q * S + 2 * p + 1]),
+                                      acc[q % GW][p]);
+      }
+    }
+}
+
+template <int S, int G, int RB, bool TANH, bool EXACT>
+__device__ __forceinline__ void run_split_group(const GroupSplit& gr, const uint32_t* __restrict__ off_s,
+                                                const float* __restrict__ w_s, const StepT<float>* __restrict__ st,
+                                                char* vb, uint32_t tlane, uint32_t cmask) {
+  constexpr int GW = G == 3 ? 4 : G;
+  constexpr int SP = (S + 1) / 2;
+  using PackT = Pack<float, S>;
+  float2 acc[G][SP];
+#pragma unroll
+  for (int j = 0; j < G; ++j)
+#pragma unroll
+    for (int p = 0; p < SP; ++p) acc[j][p] = make_float2(0.0f, 0.0f);
+  {  // input block: TMEM columns, two rounds per wait::ld
+    const uint32_t* op = off_s + gr.e_in;
+    const float* wp = w_s + gr.e_in;
+#pragma unroll 1
+    for (int r = 0; r < gr.rounds_in; r += 2) {
+      uint32_t c[2 * GW];
+      float w[2 * GW];
+      float v[2 * GW * S];
+      load_u32<2 * GW>(op + r * GW, c);
+      load_f32<2 * GW>(wp + r * GW, w);
+      input_issue<S, G, GW>(v, c, tlane, cmask);
+      tmem_wait_ld(v);
+      input_fma<S, G, GW, EXACT>(acc, v, w, r, gr.cnt_in);
+    }
+  }
+  {  // hidden block: shared-memory slots, double-buffered program words
+    const uint32_t* op = off_s + gr.e_h;
+    const float* wp = w_s + gr.e_h;
+    const int rounds = gr.rounds_h;
+    uint32_t oa[2 * GW], ob[2 * GW];
+    float wa[2 * GW], wb[2 * GW];
+    if (rounds > 0) {
+      load_u32<2 * GW>(op, oa);
+      load_f32<2 * GW>(wp, wa);
+    }
+#pragma unroll 1
+    for (int r = 0; r < rounds; r += 4) {
+      load_u32<2 * GW>(op + (r + 2) * GW, ob);
+      load_f32<2 * GW>(wp + (r + 2) * GW, wb);
+      sum_rounds<S, G, GW>(acc, oa, wa, vb);
+      if (r + 2 >= rounds) break;
+      load_u32<2 * GW>(op + (r + 4) * GW, oa);
+      load_f32<2 * GW>(wp + (r + 4) * GW, wa);
+      sum_rounds<S, G, GW>(acc, ob, wb, vb);
+    }
+  }
+  if constexpr (TANH) {
+    constexpr float K = -2.8853900817779268f;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const StepT<float> sj = st[j];
+      const float rk = sj.resp * K, bk = sj.bias * K;
+      PackT y;
+      if constexpr (S == 1) {
+        y.v[0] = fmaf(2.0f, rcp_approx(1.0f + ex2_approx(fmaf(rk, acc[j][0].x, bk))), -1.0f);
+      } else {
+#pragma unroll
+        for (int p = 0; p < SP; ++p) {
+          const float2 t = __ffma2_rn(make_float2(rk, rk), acc[j][p], make_float2(bk, bk));
+          const float2 d = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(ex2_approx(t.x), ex2_approx(t.y)));
+          const float2 yy = __ffma2_rn(make_float2(2.0f, 2.0f), make_float2(rcp_approx(d.x), rcp_approx(d.y)),
+                                       make_float2(-1.0f, -1.0f));
+          y.v[2 * p] = yy.x;
+          y.v[2 * p + 1] = yy.y;
+        }
+      }
+      if (sj.slot != NO_SLOT) *reinterpret_cast<PackT*>(vb + sj.slot * RB) = y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      float a[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) a[s] = (s & 1) ? acc[j][s / 2].y : acc[j][s / 2].x;
+      finish_step<S, RB>(st[j], a, vb);
+    }
+  }
+}
+
+// non-sum singleton (product / max / min): exact counts in both blocks
+template <int S, int RB>
+__device__ __forceinline__ void run_split_generic(const GroupSplit& gr, const uint32_t* __restrict__ off_s,
+                                                  const float* __restrict__ w_s, const StepT<float>& st, char* vb,
+                                                  uint32_t tlane) {
+  float acc[S];
+  const float neutral = agg_neutral<float>(st.agg);
+#pragma unroll
+  for (int s = 0; s < S; ++s) acc[s] = neutral;
+  for (int e = 0; e < gr.cnt_in[0]; ++e) {
+    float v[S];
+    tmem_ld_cols<S>(tlane + off_s[gr.e_in + e], v);
+    tmem_wait_ld(v);
+    const float w = w_s[gr.e_in + e];
+#pragma unroll
+    for (int s = 0; s < S; ++s) acc[s] = agg_combine<float>(st.agg, acc[s], w * v[s]);
+  }
+  for (int e = 0; e < gr.cnt_h[0]; ++e) {
+    const Pack<float, S> v = *reinterpret_cast<const Pack<float, S>*>(vb + off_s[gr.e_h + e]);
+    const float w = w_s[gr.e_h + e];
+#pragma unroll
+    for (int s = 0; s < S; ++s) acc[s] = agg_combine<float>(st.agg, acc[s], w * v.v[s]);
+  }
+  if (st.count == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) acc[s] = 0.0f;
+  }
+  StepT<float> sum_like = st;
+  sum_like.agg = AGG_SUM;
+  finish_step<S, RB>(sum_like, acc, vb);
+}
+
+template <int S, int RB, bool EXACT>
+__device__ __forceinline__ void split_sweep(const GroupSplit* gr_s, int n_groups, const uint32_t* off_s,
+                                            const float* w_s, const StepT<float>* st_s, char* vb, uint32_t tlane,
+                                            uint32_t cmask) {
+#pragma unroll 1
+  for (int g = 0; g < n_groups; ++g) {
+    const GroupSplit gr = decode_group(gr_s, g);
+    const StepT<float>* st = st_s + gr.step_begin;
+    if (gr.cls & GRP_GENERIC) {
+      run_split_generic<S, RB>(gr, off_s, w_s, st[0], vb, tlane);
+    } else if (gr.cls & GRP_TANH_SUM) {
+      switch (gr.n) {
+        case 1: run_split_group<S, 1, RB, true, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
+        case 2: run_split_group<S, 2, RB, true, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
+        case 3: run_split_group<S, 3, RB, true, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
+        default: run_split_group<S, 4, RB, true, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
+      }
+    } else {
+      switch (gr.n) {
+        case 1: run_split_group<S, 1, RB, false, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
+        case 2: run_split_group<S, 2, RB, false, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
+        case 3: run_split_group<S, 3, RB, false, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
+        default: run_split_group<S, 4, RB, false, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
+      }
+    }
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(SPLIT_NT, TNEAT_SPLIT_WARPS / 4)
+fwd_split_kernel(const uint8_t* __restrict__ prog, ProgLayout L, const int32_t* __restrict__ genome_ids,
+                 const float* __restrict__ in, int64_t in_gstride, int B, int I, int O, int runs, int tpc,
+                 uint32_t tcols, float* __restrict__ out, int64_t out_gstride) {
+  constexpr int TT = SPLIT_NT * S;
+  constexpr int RB = (TT + S) * 4;  // bytes of one hidden value slot row (padded by S)
+  using PackT = Pack<float, S>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t tmem_base;
+  __shared__ uint16_t oslot[8];
+  const int64_t task = blockIdx.x / runs;
+  const int run = (int)(blockIdx.x - task * runs);
+  const int64_t gi = genome_ids ? (int64_t)__ldg(genome_ids + task) : task;
+  const uint8_t* gp = prog + gi * L.stride;
+  const ProgHeader hdr = *reinterpret_cast<const ProgHeader*>(gp);
+  const int n_steps = hdr.n_steps, n_edges = hdr.n_edges, n_groups = hdr.n_groups;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const float* gin = in + gi * in_gstride;
+  const bool vec_in = (I & 3) == 0 && (((uintptr_t)gin) & 15) == 0;
+  if (tid == 0 && vec_in) {
+    const int t0 = run * tpc * TT;
+    if (t0 < B) prefetch_l2(gin + (int64_t)t0 * I, (uint32_t)(min(TT, B - t0) * I * 4));
+  }
+  // shared memory: groups | steps | u32 offsets | weights | hidden values [slot][TT + S]
+  GroupSplit* gr_s = reinterpret_cast<GroupSplit*>(smem);
+  const int64_t off_st = (int64_t)n_groups * sizeof(GroupSplit);
+  StepT<float>* st_s = reinterpret_cast<StepT<float>*>(smem + off_st);
+  const int64_t off_src = off_st + (int64_t)n_steps * sizeof(StepT<float>);
+  uint32_t* off_s = reinterpret_cast<uint32_t*>(smem + off_src);
+  const int64_t off_w = off_src + align_up(4ll * n_edges, 16);
+  float* w_s = reinterpret_cast<float*>(smem + off_w);
+  float* vals = reinterpret_cast<float*>(smem + align_up(off_w + 4ll * n_edges, 16));
+
+  if (warp == 0) {
+    tmem_alloc(smem_u32(&tmem_base), tcols);
+    tmem_relinquish();
+  }
+  {
+    auto copy16 = [&](void* dst, const void* src, int64_t bytes) {
+      const int n16 = (int)(bytes / 16);
+      for (int i = tid; i < n16; i += SPLIT_NT)
+        reinterpret_cast<int4*>(dst)[i] = __ldg(reinterpret_cast<const int4*>(src) + i);
+    };
+    copy16(gr_s, gp + L.off_groups, off_st);
+    copy16(st_s, gp + L.off_steps, (int64_t)n_steps * sizeof(StepT<float>));
+    copy16(w_s, gp + L.off_w, 4ll * n_edges);
+    const uint32_t* gs = reinterpret_cast<const uint32_t*>(gp + L.off_src);  // raw u16 pairs
+    for (int i = tid; i < n_edges / 2; i += SPLIT_NT) {
+      const uint32_t pr = __ldg(gs + i);
+      reinterpret_cast<uint2*>(off_s)[i] = make_uint2(pr & 0xFFFFu, pr >> 16);
+    }
+  }
+  const uint16_t* os = reinterpret_cast<const uint16_t*>(gp + L.off_out);
+  if (tid < 8) oslot[tid] = tid < O ? __ldg(os + tid) : NO_SLOT;
+  if (hdr.n_slots > 0)
+    for (int i = tid; i < TT + S; i += SPLIT_NT) vals[(int64_t)(hdr.n_slots - 1) * (RB / 4) + i] = 0.0f;
+  __syncthreads();
+  // scale the raw sources: input blocks -> TMEM column offset k*S, hidden blocks -> byte offset slot*RB
+  for (int g = tid; g < n_groups; g += SPLIT_NT) {
+    const GroupSplit gr = gr_s[g];
+    const int gw = group_width(gr.n);
+    for (int e = gr.e_in; e < gr.e_in + gw * gr.rounds_in; ++e) off_s[e] *= (uint32_t)S;
+    for (int e = gr.e_h; e < gr.e_h + gw * gr.rounds_h; ++e) off_s[e] *= (uint32_t)RB;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tlane = tmem_base + ((uint32_t)(warp * 32) << 16);
+  char* vb = reinterpret_cast<char*>(vals) + tid * S * 4;
+  bool fast_out = O == 8;
+#pragma unroll
+  for (int o = 0; o < 8; ++o) fast_out = fast_out && oslot[o] != NO_SLOT;
+  float* go = out + gi * out_gstride;
+  const int tile_end = min((run + 1) * tpc, (B + TT - 1) / TT);
+  for (int tile = run * tpc; tile < tile_end; ++tile) {
+    const int t0 = tile * TT;
+    if (tid == 0 && vec_in && tile + 1 < tile_end) {
+      const int t1 = t0 + TT;
+      prefetch_l2(gin + (int64_t)t1 * I, (uint32_t)(min(TT, B - t1) * I * 4));
+    }
+    const int s0 = t0 + tid * S;
+    // own input rows -> TMEM lane (column k*S + s), eight columns per store
+    float2 nf = make_float2(0.0f, 0.0f);  // x * 0 sums: NaN iff some input is not finite
+    for (int k0 = 0; k0 < I; k0 += 8 / S) {
+      float c[8];
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const bool ok = s0 + s < B;
+        const float* row = gin + (int64_t)(ok ? s0 + s : 0) * I + k0;
+#pragma unroll
+        for (int kk = 0; kk < 8 / S; ++kk) c[kk * S + s] = 0.0f;
+        if (ok) {
+          if (vec_in) {
+#pragma unroll
+            for (int h = 0; h < 8 / S; h += 4) {
+              if (k0 + h < I) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(row + h));
+                c[(h + 0) * S + s] = x.x; c[(h + 1) * S + s] = x.y; c[(h + 2) * S + s] = x.z; c[(h + 3) * S + s] = x.w;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < 8 / S; ++kk)
+              if (k0 + kk < I) c[kk * S + s] = __ldg(row + kk);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) nf = __ffma2_rn(make_float2(c[q], c[q + 1]), make_float2(0.0f, 0.0f), nf);
+      tmem_st8(tlane + (uint32_t)(k0 * S), c);
+    }
+    tmem_wait_st();
+    const bool exact = __any_sync(0xffffffffu, nf.x != nf.x || nf.y != nf.y);
+    if (exact) split_sweep<S, RB, true>(gr_s, n_groups, off_s, w_s, st_s, vb, tlane, tcols - 1);
+    else split_sweep<S, RB, false>(gr_s, n_groups, off_s, w_s, st_s, vb, tlane, tcols - 1);
+
+    if (fast_out) {
+      PackT v[8];
+#pragma unroll
+      for (int o = 0; o < 8; ++o) v[o] = *reinterpret_cast<const PackT*>(vb + (uint32_t)oslot[o] * RB);
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        if (s0 + j >= B) break;
+        float4* row = reinterpret_cast<float4*>(go + (int64_t)(s0 + j) * 8);
+        row[0] = make_float4(v[0].v[j], v[1].v[j], v[2].v[j], v[3].v[j]);
+        row[1] = make_float4(v[4].v[j], v[5].v[j], v[6].v[j], v[7].v[j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        if (s0 + j >= B) break;
+        float* row = go + (int64_t)(s0 + j) * O;
+        for (int o = 0; o < O; ++o) {
+          const uint16_t sl = __ldg(os + o);
+          row[o] = sl != NO_SLOT ? *reinterpret_cast<const float*>(vb + sl * RB + j * 4) : NAN;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, tcols);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // warp-per-(genome, input chunk) kernel for small batches
 // ---------------------------------------------------------------------------
 
@@ -721,6 +1081,35 @@ int launch_tile(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, co
   return 0;
 }
 
+// split programs: maxdims_host = (hidden slots incl. zero slot, steps, edge entries)
+// maxima over the launched genomes
+int launch_split(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, const float* in,
+                 int64_t in_gstride, int64_t P, int B, int I, int O, const int32_t* maxdims_host, float* out,
+                 int64_t out_gstride, int tpc, cudaStream_t st) {
+  constexpr int S = 2, TT = SPLIT_NT * S, RB = (TT + S) * 4;
+  if (I * S > 512) return -8;
+  const int tiles = (B + TT - 1) / TT;
+  tpc = max(1, min(tpc, tiles));
+  const int runs = (tiles + tpc - 1) / tpc;
+  const int64_t grid = P * runs;
+  if (grid > 0x7FFFFFFFll) return -5;
+  const int64_t slots = maxdims_host[0] > 1 ? maxdims_host[0] : 1, ms = maxdims_host[1], me = maxdims_host[2];
+  uint32_t tcols = 32;
+  while (tcols < (uint32_t)(I * S)) tcols <<= 1;
+  int64_t smem = align_up(32 * ms + 16 * ms, 16) + align_up(4 * me, 16) + align_up(4 * me, 16) + slots * RB;
+  // no more resident CTAs per SM than the TMEM columns allow (an allocation
+  // that does not fit would spin until another CTA on the SM exits)
+  const int tmem_ctas = 512 / (int)tcols;
+  const int64_t smem_floor = (228ll * 1024) / (tmem_ctas + 1) - 1024 + 64;
+  if (smem < smem_floor) smem = smem_floor;
+  if (smem > 227 * 1024) return -6;
+  cudaFuncSetAttribute(fwd_split_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  fwd_split_kernel<S><<<(unsigned)grid, SPLIT_NT, smem, st>>>(prog, L, ids, in, in_gstride, B, I, O, runs, tpc,
+                                                               tcols, out, out_gstride);
+  TNEAT_CHECK_LAUNCH();
+  return 0;
+}
+
 }  // namespace tneat
 
 using namespace tneat;
@@ -742,21 +1131,27 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
   const int64_t ogs = (int64_t)B * O;
   // variant (low 4 bits): 0 = auto, 1 = tile S=1 (128 thr), 2 = tile S=2 (128 thr),
   // 3 = tile S=1 (64 thr), 4 = tile S=4 (64 thr), 5 = tile S=2 (64 thr), 6 = tile S=4 (32 thr),
-  // 8 = warp kernel; bits 8..15 = tiles per CTA (0 = default 4)
+  // 8 = warp kernel, 10 = split kernel (split programs: the only one, and auto);
+  // bits 8..15 = tiles per CTA (0 = default 4)
   int tpc = (variant >> 8) & 0xFF;
   if (tpc == 0) tpc = 4;
   variant &= 0xF;
+  if (precision & FMT_SPLIT) {  // split programs run on the split kernel only
+    if (variant != 0 && variant != 10) return -7;
+    return launch_split(pg, L, genome_ids, (const float*)inputs, input_genome_stride, P, B, I, O, maxdims_host,
+                        (float*)outputs, ogs, tpc, st);
+  }
   if (variant == 0) variant = B >= 192 ? 5 : (B >= 96 ? 3 : 8);
   if (variant == 8) {
     if (genome_ids) return -7;
-    if (precision)
+    if (precision & FMT_F64)
       return launch_warp<double>(pg, L, P, (const double*)inputs, input_genome_stride, B, I, O, maxdims_host,
                                  (double*)outputs, ogs, FIT_NONE, nullptr, nullptr, st);
     return launch_warp<float>(pg, L, P, (const float*)inputs, input_genome_stride, B, I, O, maxdims_host,
                               (float*)outputs, ogs, FIT_NONE, nullptr, nullptr, st);
   }
   const int32_t* ids = genome_ids;
-  if (precision) {
+  if (precision & FMT_F64) {
     const double* in = (const double*)inputs;
     double* out = (double*)outputs;
     if (variant == 2 || variant == 5)
@@ -784,6 +1179,7 @@ int an_forward_fitness(const void* program, int64_t program_stride, int N, int C
   if (P < 0 || B < 1 || I < 1 || O != 1 || !maxdims_host || (kind != 1 && kind != 2)) return -1;
   if (kind == 1 && B != 4) return -1;
   if (kind == 2 && !targets) return -2;
+  if (precision & FMT_SPLIT) return -7;
   if (P == 0) return 0;
   const ProgLayout L = prog_layout(N, C, O, precision);
   if (L.stride != program_stride) return -3;
@@ -801,6 +1197,7 @@ int an_cartpole(const void* program, int64_t program_stride, int N, int C, int p
                 const int32_t* maxdims_host, int64_t P, const double* start, int max_steps, double* fitness,
                 void* stream) {
   if (P < 0 || !maxdims_host || max_steps < 0) return -1;
+  if (precision & FMT_SPLIT) return -7;
   if (P == 0) return 0;
   const ProgLayout L = prog_layout(N, C, 1, precision);
   if (L.stride != program_stride) return -3;

@@ -44,7 +44,8 @@ struct WarpSmem {
   uint16_t* slot_of;  // [N]
   uint16_t* step_row; // [N]
   uint16_t* grp_of;   // [N]
-  GroupRec* grp;      // [N]
+  GroupRec* grp;      // [N]      (standard programs)
+  GroupSplit* grps;   // [N]      (split programs; same memory as grp)
   uint8_t* flags;     // [N]
   uint8_t* needed;    // [N]
   uint8_t* used;      // [N]
@@ -59,7 +60,7 @@ __host__ __device__ inline int next_pow2(int x) {
 }
 
 template <bool kCarve>
-__host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, WarpSmem* s) {
+__host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, bool split, WarpSmem* s) {
   const int Npad = next_pow2(N), Cpad = next_pow2(C);
   const int W = (N + 31) / 32, WS = (N + 2 + 31) / 32;
   int64_t o = 0;
@@ -74,7 +75,7 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, Warp
   // the arrays that are first written after Kahn (gkey, grp, last_grp,
   // step_row, grp_of)
   const int64_t a_union = take(0, 16);
-  const int64_t a_gkey = take(8ll * Npad, 8), a_grp = take(16ll * N, 16), a_last = take(4ll * N, 4);
+  const int64_t a_gkey = take(8ll * Npad, 8), a_grp = take((split ? 32ll : 16ll) * N, 16), a_last = take(4ll * N, 4);
   const int64_t a_srow = take(2ll * N, 2), a_grpof = take(2ll * N, 2);
   const int64_t a_ekey2 = a_union;
   o = a_union + (o - a_union > 8ll * (C > 0 ? C : 1) ? o - a_union : 8ll * (C > 0 ? C : 1));
@@ -96,6 +97,7 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, Warp
     s->lvl = (int32_t*)(base + a_lvl);
     s->last_grp = (int32_t*)(base + a_last);
     s->grp = (GroupRec*)(base + a_grp);
+    s->grps = (GroupSplit*)(base + a_grp);
     s->succ = (uint16_t*)(base + a_succ);
     s->order = (uint16_t*)(base + a_order);
     s->slot_of = (uint16_t*)(base + a_slot);
@@ -110,7 +112,9 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, Warp
   return align_up(o, 16);
 }
 
-__host__ inline int64_t warp_smem_bytes(int N, int C) { return layout_warp<false>(nullptr, N, C, nullptr); }
+__host__ inline int64_t warp_smem_bytes(int N, int C, bool split) {
+  return layout_warp<false>(nullptr, N, C, split, nullptr);
+}
 
 // ascending bitonic sort of n (power of two, >= 32) u64 values, one warp
 __device__ void warp_bitonic_sort(uint64_t* a, int n) {
@@ -178,7 +182,7 @@ __device__ inline int warp_first_set(const uint32_t* words, int nw) {
 
 template <typename T>
 __global__ void transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
-                                 int64_t P, int N, int C, int I, int O, int mode, int prune,
+                                 int64_t P, int N, int C, int I, int O, int mode, int prune, bool split,
                                  int64_t wsmem, uint8_t* __restrict__ prog, ProgLayout L,
                                  int16_t* __restrict__ order_out, int16_t* __restrict__ conn_rows,
                                  int32_t* __restrict__ io_rows, int32_t* __restrict__ status_out,
@@ -189,7 +193,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (g >= P) return;
   WarpSmem s;
-  layout_warp<true>(smem + warp * wsmem, N, C, &s);
+  layout_warp<true>(smem + warp * wsmem, N, C, split, &s);
   const int Npad = next_pow2(N);
   const double* gn = nodes + g * (int64_t)N * 5;
   const double* gc = conns + g * (int64_t)C * 4;
@@ -383,7 +387,14 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       if (!(gv >= 0.0 && gv < AGG_COUNT && gv == floor(gv))) bad |= ST_BAD_AGG;
       const int agg = (gv >= 0.0 && gv < AGG_COUNT) ? (int)gv : 0;
       const uint64_t cls = (recurrent || !(agg == AGG_SUM || agg == AGG_MEAN)) ? 1 : 0;
-      const uint64_t cnt = (uint64_t)(s.in_start[r + 1] - s.in_start[r]);
+      uint64_t cnt = (uint64_t)(s.in_start[r + 1] - s.in_start[r]);
+      if (split) {  // split programs group by the input-edge count (outdeg: free since the CSR build)
+        int cin = 0;
+        for (int e = s.in_start[r]; e < s.in_start[r + 1]; ++e)
+          cin += (s.flags[(int)((s.ekey[e] >> 32) & 0xFFFF)] & F_INPUT) ? 1 : 0;
+        s.outdeg[r] = cin;
+        cnt = (uint64_t)cin;
+      }
       const uint64_t lv = recurrent ? 0 : (uint64_t)s.lvl[r];
       s.gkey[n_emit + __popc(me & ((1u << lane) - 1))] =
           (lv << 48) | (cls << 47) | ((0xFFFFull - cnt) << 16) | (uint64_t)i;
@@ -399,7 +410,57 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   // group formation (sequential, lane 0): same level & class, <= 4 steps, and
   // a step joins only if its list is at least half the group's longest list
   // (bounds the padded edge entries, see edge_capacity)
-  if (lane == 0) {
+  if (lane == 0 && split) {
+    // split programs: the join rule bounds the input block; the hidden block
+    // is padded to the group's longest hidden list (edge_capacity_split)
+    int ng = 0, e_total = 0;
+    int cur_lv = -1, cur_cls = -1, cur_rounds = 0;
+    auto close = [&](GroupSplit& gr) {
+      const int gw = group_width(gr.n);
+      if (!(gr.cls & GRP_GENERIC)) {
+        gr.rounds_in = (uint16_t)((gr.rounds_in + 1) & ~1);
+        gr.rounds_h = (uint16_t)((gr.rounds_h + 1) & ~1);
+      }
+      gr.e_in = (uint16_t)e_total;
+      e_total = (int)align_up(e_total + gw * gr.rounds_in, 8);
+      gr.e_h = (uint16_t)e_total;
+      e_total = (int)align_up(e_total + gw * gr.rounds_h, 8);
+    };
+    for (int k = 0; k < n_emit; ++k) {
+      const uint64_t key = s.gkey[k];
+      const int pos = (int)(key & 0xFFFF);
+      const int row = (int)s.order[pos];
+      const int cin = 0xFFFF - (int)((key >> 16) & 0xFFFF);
+      const int ch = s.in_start[row + 1] - s.in_start[row] - cin;
+      const int cls = (int)((key >> 47) & 1);
+      const int lv = (int)(key >> 48);
+      const bool join = ng > 0 && lv == cur_lv && cls == cur_cls && cls == 0 && s.grps[ng - 1].n < 4 &&
+                        TNEAT_JOIN_DEN * cin >= TNEAT_JOIN_NUM * cur_rounds;
+      if (!join) {
+        if (ng > 0) close(s.grps[ng - 1]);
+        GroupSplit gr;
+        memset(&gr, 0, sizeof(gr));
+        gr.cls = (uint8_t)cls;
+        gr.rounds_in = (uint16_t)cin;
+        gr.step_begin = (uint16_t)k;
+        s.grps[ng++] = gr;
+        cur_lv = lv; cur_cls = cls; cur_rounds = cin;
+      }
+      GroupSplit& gr = s.grps[ng - 1];
+      gr.cnt_in[gr.n] = (uint16_t)cin;
+      gr.cnt_h[gr.n] = (uint16_t)ch;
+      if (ch > gr.rounds_h) gr.rounds_h = (uint16_t)ch;
+      const bool tanh_sum = gn[(int64_t)row * 5 + 4] == (double)ACT_TANH && gn[(int64_t)row * 5 + 3] == (double)AGG_SUM;
+      if (gr.n == 0) gr.cls |= tanh_sum ? GRP_TANH_SUM : 0;
+      else if (!tanh_sum) gr.cls &= ~GRP_TANH_SUM;
+      gr.n++;
+      s.step_row[k] = (uint16_t)row;
+      s.grp_of[k] = (uint16_t)(ng - 1);
+    }
+    if (ng > 0) close(s.grps[ng - 1]);
+    s.ready[0] = (uint32_t)ng;
+    s.indeg[0] = e_total;
+  } else if (lane == 0) {
     int ng = 0, e_total = 0;
     int cur_lv = -1, cur_cls = -1, cur_rounds = 0;
     for (int k = 0; k < n_emit; ++k) {
@@ -452,19 +513,22 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   }
   // slots: 0..I-1 hold the inputs, the rest start free; one more slot after
   // the last allocated one is the zero slot read by padding entries
+  // (split programs: inputs take no slot, hidden slots number from 0)
   const int WS = (N + 2 + 31) / 32;
+  const int first_free = split ? 0 : I;
   for (int w = lane; w < WS; w += 32) {
     uint32_t m = 0;
     for (int b = 0; b < 32; ++b) {
       const int sl = w * 32 + b;
-      if (sl >= I && sl < N + 2) m |= 1u << b;
+      if (sl >= first_free && sl < N + 2) m |= 1u << b;
     }
     s.freemask[w] = m;
   }
-  for (int r = lane; r < N; r += 32)
-    if (s.flags[r] & F_INPUT) s.slot_of[r] = (uint16_t)gn[(int64_t)r * 5];
+  if (!split)
+    for (int r = lane; r < N; r += 32)
+      if (s.flags[r] & F_INPUT) s.slot_of[r] = (uint16_t)gn[(int64_t)r * 5];
   __syncwarp();
-  int n_slots = I;
+  int n_slots = first_free;
   for (int gi = 0; gi < n_groups; ++gi) {
     // recycle the slots whose last reader is this group (reads precede writes)
     if (!recurrent) {
@@ -477,9 +541,10 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       }
       __syncwarp();
     }
-    const GroupRec gr = s.grp[gi];
-    for (int j = 0; j < gr.n; ++j) {
-      const int row = s.step_row[gr.step_begin + j];
+    const int gn_steps = split ? s.grps[gi].n : s.grp[gi].n;
+    const int g_begin = split ? s.grps[gi].step_begin : s.grp[gi].step_begin;
+    for (int j = 0; j < gn_steps; ++j) {
+      const int row = s.step_row[g_begin + j];
       if (!(s.used[row] || (s.flags[row] & F_OUTPUT))) continue;
       const int sl = warp_first_set(s.freemask, WS);
       __syncwarp();
@@ -494,10 +559,62 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   const uint32_t zero_slot = (uint32_t)n_slots;
   n_slots += 1;
   // ---- write groups, steps and interleaved edge lists --------------------------
-  GroupRec* pg = (GroupRec*)(gp + L.off_groups);
   StepT<T>* steps = (StepT<T>*)(gp + L.off_steps);
-  for (int gi = lane; gi < n_groups; gi += 32) pg[gi] = s.grp[gi];
-  for (int k = lane; k < n_emit; k += 32) {
+  if (split) {
+    GroupSplit* pg = (GroupSplit*)(gp + L.off_groups);
+    for (int gi = lane; gi < n_groups; gi += 32) pg[gi] = s.grps[gi];
+    uint16_t* esrc = (uint16_t*)(gp + L.off_src);
+    float* ew = (float*)(gp + L.off_w);
+    for (int k = lane; k < n_emit; k += 32) {
+      const int row = s.step_row[k];
+      const GroupSplit gr = s.grps[s.grp_of[k]];
+      const int j = k - gr.step_begin, gw = group_width(gr.n);
+      const double* nr = gn + (int64_t)row * 5;
+      const double av = nr[4], gv = nr[3];
+      StepT<T> st;
+      memset(&st, 0, sizeof(st));
+      const int e0 = s.in_start[row], cnt = s.in_start[row + 1] - e0;
+      st.slot = (s.used[row] || (s.flags[row] & F_OUTPUT)) ? s.slot_of[row] : NO_SLOT;
+      st.act = (uint8_t)((av >= 0.0 && av < ACT_COUNT) ? (int)av : 0);
+      st.agg = (uint8_t)((gv >= 0.0 && gv < AGG_COUNT) ? (int)gv : 0);
+      st.count = (uint16_t)cnt;
+      st.bias = (T)nr[1];
+      st.resp = (T)nr[2];
+      steps[k] = st;
+      // holes: input block -> (input 0, 0.0), hidden block -> (zero slot, 0.0);
+      // the spare column of a 3-group is all holes
+      const int ncol = (gr.n == 3 && j == 2) ? 2 : 1;
+      for (int col = j; col < j + ncol; ++col) {
+        for (int rr = 0; rr < gr.rounds_in; ++rr) {
+          esrc[gr.e_in + rr * gw + col] = 0;
+          ew[gr.e_in + rr * gw + col] = 0.0f;
+        }
+        for (int rr = 0; rr < gr.rounds_h; ++rr) {
+          esrc[gr.e_h + rr * gw + col] = (uint16_t)zero_slot;
+          ew[gr.e_h + rr * gw + col] = 0.0f;
+        }
+      }
+      int ri = 0, rh = 0;  // source-row order inside each block
+      for (int e = e0; e < e0 + cnt; ++e) {
+        const uint64_t kk = s.ekey[e];
+        const int sr = (int)((kk >> 32) & 0xFFFF);
+        const float w = (float)gc[(int64_t)(kk & 0xFFFFFFFFu) * 4 + 3];
+        if (s.flags[sr] & F_INPUT) {
+          const int idx = gr.e_in + (ri++) * gw + j;
+          esrc[idx] = (uint16_t)gn[(int64_t)sr * 5];
+          ew[idx] = w;
+        } else {
+          const int idx = gr.e_h + (rh++) * gw + j;
+          esrc[idx] = s.slot_of[sr];
+          ew[idx] = w;
+        }
+      }
+    }
+  }
+  GroupRec* pg = (GroupRec*)(gp + L.off_groups);
+  if (!split)
+    for (int gi = lane; gi < n_groups; gi += 32) pg[gi] = s.grp[gi];
+  for (int k = lane; k < n_emit && !split; k += 32) {
     const int row = s.step_row[k];
     const GroupRec gr = s.grp[s.grp_of[k]];
     const int j = k - gr.step_begin, gw = group_width(gr.n);
@@ -568,29 +685,31 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
                  int mode, int precision, int prune, void* program, int64_t program_stride,
                  int16_t* order, int16_t* conn_rows, int32_t* io_rows, int32_t* status,
                  int32_t* maxdims, void* stream) {
-  if (P < 0 || N < 1 || N > 32767 || C < 0 || edge_capacity(N, C) > 65535 || I < 1 || O < 1 || I + O > N)
-    return -1;
+  const bool split = (precision & FMT_SPLIT) != 0;
+  if (P < 0 || N < 1 || N > 32767 || C < 0 || I < 1 || O < 1 || I + O > N) return -1;
+  if ((split ? edge_capacity_split(N, C) : edge_capacity(N, C)) > 65535) return -1;
+  if (split && ((precision & FMT_F64) || mode != 0)) return -1;  // split: fp32 feed-forward only
   if (!nodes || !program || !maxdims || (C > 0 && !conns)) return -2;
   const ProgLayout L = prog_layout(N, C, O, precision);
   if (program_stride != L.stride) return -3;
   if (P == 0) return 0;
   const int Cc = C > 0 ? C : 1;
-  const int64_t ws = warp_smem_bytes(N, Cc);
+  const int64_t ws = warp_smem_bytes(N, Cc, split);
   if (ws > 200 * 1024) return -4;  // genome capacity too large for one warp's shared memory
   int wpb = 4;
   while (wpb > 1 && ws * wpb > 160 * 1024) wpb >>= 1;
   const int64_t smem = ws * wpb;
   const int64_t blocks = (P + wpb - 1) / wpb;
   cudaStream_t st = (cudaStream_t)stream;
-  if (precision) {
+  if (precision & FMT_F64) {
     cudaFuncSetAttribute(transform_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     transform_kernel<double><<<(unsigned)blocks, 32 * wpb, smem, st>>>(
-        nodes, conns, P, N, C, I, O, mode, prune, ws, (uint8_t*)program, L, order, conn_rows,
+        nodes, conns, P, N, C, I, O, mode, prune, split, ws, (uint8_t*)program, L, order, conn_rows,
         io_rows, status, maxdims);
   } else {
     cudaFuncSetAttribute(transform_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     transform_kernel<float><<<(unsigned)blocks, 32 * wpb, smem, st>>>(
-        nodes, conns, P, N, C, I, O, mode, prune, ws, (uint8_t*)program, L, order, conn_rows,
+        nodes, conns, P, N, C, I, O, mode, prune, split, ws, (uint8_t*)program, L, order, conn_rows,
         io_rows, status, maxdims);
   }
   TNEAT_CHECK_LAUNCH();

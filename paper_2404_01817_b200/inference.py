@@ -17,6 +17,12 @@ Precision: ``precision="f32"`` (default) evaluates in float32 -- the north-star
 path, parity ``|d| <= 1e-5 * max(1, |ref|)`` against the float64 reference;
 ``precision="f64"`` evaluates in float64 for reference-exact checking
 (<= 1e-9 like the reference's own oracle tests, test_oracle.py:82-92).
+
+Layout: ``transform_arrays(..., layout="split")`` compiles fp32 feed-forward
+programs for the split forward kernel (input values in tensor memory, hidden
+values in shared memory; csrc/forward.cu ``fwd_split_kernel``).  It is opt-in:
+``layout="auto"`` (default) gives standard programs, which every kernel takes
+(tile / warp forward, fused fitness, cart-pole, recurrent rollouts).
 """
 
 from __future__ import annotations
@@ -34,7 +40,9 @@ from .functions import DEFAULT_REGISTRY, check_registry
 
 ST_CYCLIC, ST_BAD_ACT, ST_BAD_AGG, ST_BAD_KEY, ST_DANGLING, ST_MISSING_IO = 1, 2, 4, 8, 16, 32
 _PREC = {"f32": 0, "f64": 1}
-_TORCH_DT = {0: torch.float32, 1: torch.float64}
+FMT_F64, FMT_SPLIT = 1, 2  # program format bits (csrc/common.cuh)
+_TORCH_DT = {0: torch.float32, 1: torch.float64, 2: torch.float32}
+V_SPLIT = 10  # forward variant of split programs (inputs in TMEM)
 
 
 def _precision_code(precision) -> int:
@@ -57,7 +65,7 @@ class StackedNetworks:
     io_rows: torch.Tensor            # (P, I+O) int32
     status_dev: torch.Tensor         # (P,) int32
     maxdims: tuple[int, int, int]    # max (slots, steps, edges) over the population
-    precision: int = 0
+    precision: int = 0               # program format: FMT_F64 | FMT_SPLIT bits
     mode: int = 0
     _cache: dict = field(default_factory=dict, repr=False)
 
@@ -178,7 +186,7 @@ class TransformedNetwork:
 def transform_arrays(nodes, conns, num_inputs: int, num_outputs: int, *,
                      precision: str = "f32", network_type: str = "feedforward",
                      prune: bool = True, stream: torch.cuda.Stream | None = None,
-                     sync: bool = True) -> tuple[StackedNetworks, np.ndarray]:
+                     sync: bool = True, layout: str = "auto") -> tuple[StackedNetworks, np.ndarray]:
     """Kahn transform of every genome at once (inference.py:82-147).
 
     Returns the stacked programs and the indices of cyclic genomes (their
@@ -193,6 +201,13 @@ def transform_arrays(nodes, conns, num_inputs: int, num_outputs: int, *,
     if nd.dim() != 3 or nd.shape[2] != 5 or cd.dim() != 3 or cd.shape[2] != 4 or nd.shape[0] != cd.shape[0]:
         raise ValueError(f"expected (P,N,5) and (P,C,4) tensors, got {tuple(nd.shape)}, {tuple(cd.shape)}")
     pop, n, c = int(nd.shape[0]), int(nd.shape[1]), int(cd.shape[1])
+    if layout not in ("auto", "split", "standard"):
+        raise ValueError(f"layout must be 'auto', 'split' or 'standard', got {layout!r}")
+    split_ok = prec == 0 and mode == 0 and 2 * num_inputs <= 512 and 7 * c + 24 * n + 16 <= 65535
+    if layout == "split" and not split_ok:
+        raise ConfigError("layout='split' needs fp32 feed-forward programs with <= 256 inputs")
+    if layout == "split":  # opt-in: measured slower than the tile kernel on config 2
+        prec |= FMT_SPLIT
     stride = int(_native.lib().an_program_stride(n, c, num_outputs, prec))
     dev = nd.device
     program = torch.empty((pop, stride), dtype=torch.uint8, device=dev)
@@ -291,8 +306,8 @@ def _bucket_plan(stacked: StackedNetworks, variant: int) -> list:
     key = ("plan", variant)
     if key in stacked._cache:
         return stacked._cache[key]
-    tt = _TILE_TT[variant]
-    esz = 8 if stacked.precision else 4
+    tt = _TILE_TT.get(variant, 256)
+    esz = 8 if stacked.precision & FMT_F64 else 4
     slots = stacked._cache.get("slots")
     if slots is None:
         slots = stacked.program[:, 8:12].contiguous().view(torch.int32).reshape(-1).cpu().numpy()
@@ -301,9 +316,14 @@ def _bucket_plan(stacked: StackedNetworks, variant: int) -> list:
     sorted_slots = slots[order]
     ids = torch.from_numpy(order).to(stacked.program.device)  # 4P bytes; no pinned allocation per plan
     _, ms, me = stacked.maxdims
-    prog = 32 * ms + (16 * me if stacked.precision else 8 * me + 16) + 16
-    pad = {1: 1, 2: 2, 3: 1, 4: 4, 5: 2, 6: 4}[variant]
-    occ = _SMEM_PER_SM // (prog + np.maximum(sorted_slots, stacked.num_inputs) * (tt + pad) * esz + 1024)
+    prog = 32 * ms + (16 * me if stacked.precision & FMT_F64 else 8 * me + 16) + 16
+    if variant == V_SPLIT:  # fwd_split_kernel: 4 warps, 256 inputs per tile, hidden slots only
+        prog += 16 * ms
+        occ = np.minimum(_SMEM_PER_SM // (prog + np.maximum(sorted_slots, 1) * 258 * 4 + 1024),
+                         512 // max(32, 1 << int(np.ceil(np.log2(max(1, 2 * stacked.num_inputs))))))
+    else:
+        pad = {1: 1, 2: 2, 3: 1, 4: 4, 5: 2, 6: 4}[variant]
+        occ = _SMEM_PER_SM // (prog + np.maximum(sorted_slots, stacked.num_inputs) * (tt + pad) * esz + 1024)
     plan = []
     lo = 0
     n = sorted_slots.size
@@ -338,12 +358,18 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
         raise InvalidInput(f"expected input length {stacked.num_inputs}, got {i}")
     if out is None:
         out = torch.empty((pop, b, stacked.num_outputs), dtype=dt, device=inputs.device)
-    v = (variant & 0xF) or (5 if b >= 192 else (3 if b >= 96 else 8))
+    if stacked.precision & FMT_SPLIT:
+        v = (variant & 0xF) or V_SPLIT
+        if v != V_SPLIT:
+            raise ValueError(f"split programs run on the split kernel only (variant {V_SPLIT}); transform "
+                             f"with layout='standard' for variant {v}")
+    else:
+        v = (variant & 0xF) or (5 if b >= 192 else (3 if b >= 96 else 8))
     args = (ptr(stacked.program), stacked.stride, stacked.max_nodes, stacked.max_conns, stacked.precision)
     tail = (b, i, stacked.num_outputs, ptr(out), int(variant) if variant > 15 else int(v),
             stream_handle(stream))
     v &= 0xF
-    if v in _TILE_TT and bucketed and pop > 1:
+    if (v in _TILE_TT or v == V_SPLIT) and bucketed and pop > 1:
         for ids, md in _bucket_plan(stacked, v):
             _native.call("an_forward", *args, _maxdims_arg(stacked, md), ptr(ids), ptr(inputs), gstride,
                          int(ids.numel()), *tail)

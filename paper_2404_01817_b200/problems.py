@@ -64,7 +64,7 @@ class Problem:
         check_registry(registry)
         rng = rng or RngStream(0)
         stacked, cyclic = transform_arrays(pop.nodes, pop.conns, pop.num_inputs, pop.num_outputs,
-                                           precision=self.precision)
+                                           precision=self.precision, layout="standard")
         if cyclic.size:
             _raise_cycles(cyclic, 0, f"cyclic genomes at indices {cyclic.tolist()}")
         return self.evaluate_stacked(stacked, registry, rng, indices=np.arange(stacked.size))
@@ -72,7 +72,7 @@ class Problem:
 
 def _fused(stacked: StackedNetworks, inputs: np.ndarray, kind: int, targets: np.ndarray | None) -> np.ndarray:
     _check_codes(stacked)
-    dt = torch.float64 if stacked.precision else torch.float32
+    dt = torch.float64 if stacked.precision & 1 else torch.float32
     dev = device()
     x = torch.from_numpy(np.ascontiguousarray(inputs)).to(dev, dt)
     tg = torch.from_numpy(np.ascontiguousarray(targets, dtype=np.float64)).to(dev) if targets is not None else None

@@ -41,7 +41,7 @@ def rollout_fitness(stacked: StackedNetworks, env=None, steps: int = 1000, sweep
         raise ValueError("rollouts need programs compiled with network_type='recurrent'")
     _check_codes(stacked)
     a, m, s0 = env if env is not None else ant_env(obs=stacked.num_inputs, act=stacked.num_outputs)
-    dt = torch.float64 if stacked.precision else torch.float32
+    dt = torch.float64 if stacked.precision & 1 else torch.float32
     dev = device()
     at, mt, st0 = (torch.from_numpy(np.ascontiguousarray(x)).to(dev, dt) for x in (a, m, s0))
     d = int(at.shape[0])

@@ -6,7 +6,9 @@ Tolerances (written here, per north_star):
   * f64 programs: |d| <= 1e-9 (the reference's own oracle bound, test_oracle.py:82-92);
   * f32 programs: |d| <= 1e-5 * max(1, |ref|) on the tanh/sum
     north-star networks; mixed act/agg networks (identity/product chains
-    amplify fp32 rounding) use 1e-4 * max(1, |ref|).
+    amplify fp32 rounding) use 1e-4 * max(1, |ref|).  Both program layouts --
+    "standard" (tile / warp kernels) and "split" (inputs in tensor memory,
+    fwd_split_kernel) -- meet the same bounds.
 """
 
 from __future__ import annotations
@@ -65,19 +67,24 @@ def test_forward_f32_matches_reference(tn, name, tol):
     g = load_golden(name)
     ok = np.setdiff1d(np.arange(g["nodes"].shape[0]), g["cyclic"])
     st, _ = tn.transform_arrays(g["nodes"][ok], g["conns"][ok], int(g["num_inputs"]),
-                                int(g["num_outputs"]))
+                                int(g["num_outputs"]), layout="standard")
     x = g["inputs_f32"][ok] if "inputs_f32" in g else g["inputs"][ok].astype(np.float32)
     ref = g["outputs"][ok]
     for variant in (0, 1, 2, 4, 8):
         out = tn.forward_arrays(st, None, x, variant=variant)
         assert _rel_err(out, ref) <= tol, (variant, _rel_err(out, ref))
+    sp, _ = tn.transform_arrays(g["nodes"][ok], g["conns"][ok], int(g["num_inputs"]),
+                                int(g["num_outputs"]), layout="split")
+    assert sp.precision & tn.inference.FMT_SPLIT
+    out = tn.forward_arrays(sp, None, x)
+    assert _rel_err(out, ref) <= tol, ("split", _rel_err(out, ref))
 
 
 def test_tile_variants_bitwise_equal_and_chunk_invariant(tn):
     import torch
     from oracle.arrayneat_oracle import synthetic_population
     nodes, conns = synthetic_population(40, 128, 512, 32, 8, seed=77)
-    st, _ = tn.transform_arrays(nodes, conns, 32, 8)
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8, layout="standard")
     x = torch.randn(40, 1000, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
     outs = [tn.forward_device(st, x, variant=v) for v in (1, 2, 4)]
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
@@ -87,6 +94,63 @@ def test_tile_variants_bitwise_equal_and_chunk_invariant(tn):
     assert torch.equal(part, outs[1])
     half = tn.forward_device(st, x[:, 300:700].contiguous(), variant=2)
     assert torch.equal(half, outs[1][:, 300:700])
+
+
+def test_split_chunk_invariant_and_matches_standard(tn):
+    """Split programs: genome chunks / input sub-ranges / shared inputs give
+    bitwise identical rows; results agree with the standard layout to fp32."""
+    import torch
+    from oracle.arrayneat_oracle import synthetic_population
+    nodes, conns = synthetic_population(40, 128, 512, 32, 8, seed=78)
+    sp, _ = tn.transform_arrays(nodes, conns, 32, 8, layout="split")
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8, layout="standard")
+    x = torch.randn(40, 1000, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(2))
+    full = tn.forward_device(sp, x)
+    part = torch.cat([tn.forward_device(sp.select(slice(a, a + 13)), x[a:a + 13].contiguous())
+                      for a in range(0, 40, 13)])
+    assert torch.equal(part, full)
+    half = tn.forward_device(sp, x[:, 256:700].contiguous())
+    assert torch.equal(half, full[:, 256:700])
+    ref = tn.forward_device(st, x, variant=2)
+    assert (full - ref).abs().max().item() <= 2e-5  # both within 1e-5 of the float64 reference
+    shared = tn.forward_device(sp, x[0].contiguous(), shared=True)
+    assert torch.equal(shared[0], full[0])
+
+
+@pytest.mark.parametrize("ni", [1, 3, 5, 12, 40, 64])
+def test_split_input_widths(tn, ni):
+    """TMEM column layouts for odd / small / wide input counts, scalar and
+    vector input loads, against the oracle."""
+    import torch
+    from oracle import arrayneat_oracle as orc
+    nodes, conns = orc.synthetic_population(12, 48 + ni, 160, ni, 3, seed=100 + ni, min_conns=20,
+                                            max_conns_drawn=150)
+    sp, cyc = tn.transform_arrays(nodes, conns, ni, 3, layout="split")
+    assert cyc.size == 0
+    x = np.random.default_rng(ni).standard_normal((12, 300, ni), dtype=np.float32)
+    out = tn.forward_device(sp, torch.from_numpy(x).cuda()).cpu().numpy()
+    for p in range(12):
+        tr = orc.transform_genome(nodes[p], conns[p], ni, 3)
+        ref = orc.forward_genome(nodes[p], tr, x[p].astype(np.float64))
+        assert _rel_err(out[p], ref) <= 1e-5, (p, _rel_err(out[p], ref))
+
+
+def test_split_nonfinite_inputs_match_standard(tn):
+    """A tile with an infinite input runs the exact variant (no 0 * inf from
+    padding): outputs equal the standard layout's, NaN/inf positions included."""
+    import torch
+    from oracle.arrayneat_oracle import synthetic_population
+    nodes, conns = synthetic_population(6, 128, 512, 32, 8, seed=79)
+    sp, _ = tn.transform_arrays(nodes, conns, 32, 8, layout="split")
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8, layout="standard")
+    x = torch.randn(6, 600, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(3))
+    x[1, 17, 5] = float("inf")
+    x[4, 300, 0] = -float("inf")
+    a = tn.forward_device(sp, x)
+    b = tn.forward_device(st, x, variant=2)
+    assert torch.equal(torch.isnan(a), torch.isnan(b))
+    fin = ~torch.isnan(a)
+    assert (a[fin] - b[fin]).abs().max().item() <= 2e-5
 
 
 def test_config2_shapes_against_oracle_sampled(tn):
