@@ -92,3 +92,51 @@ def test_sharded_generation_single_rank_equals_evolve_step(tn):
         assert st_a.best_fitness == st_b.best_fitness and st_a.mean_fitness == st_b.mean_fitness
     assert np.array_equal(pop.nodes.cpu().numpy(), nodes.cpu().numpy(), equal_nan=True)
     assert [s.species_key for s in species] == [s.species_key for s in sp_b]
+
+
+def test_run_experiment_artifacts_and_resume(tn, tmp_path):
+    """run_experiment writes the reference's artifacts (stats.csv schema,
+    best_genome.json, checkpoint.pkl); resuming from a mid-run checkpoint
+    reproduces the uninterrupted run exactly (runner.py:145-198)."""
+    from paper_2404_01817_b200.artifacts import load_checkpoint, parse_genome, save_checkpoint
+    from paper_2404_01817_b200.runner import EXIT_GENERATION_LIMIT, STATS_HEADER, run_experiment
+    g = load_golden("problems.npz")
+    cfg = tn.NeatConfig(seed=3, pop_size=150, generation_limit=5)
+    full = run_experiment(cfg, tmp_path / "full")
+    assert full.exit_code == EXIT_GENERATION_LIMIT and full.generations == 5
+    lines = full.stats_path.read_text().splitlines()
+    assert lines[0] == STATS_HEADER and len(lines) == 6
+    rows = np.array([[float(v) for v in ln.split(",")[1:]] for ln in lines[1:]])
+    np.testing.assert_allclose(rows[:, [0, 1, 2, 3, 4]], g["run_stats"], rtol=1e-9, atol=1e-9)
+    best = parse_genome(full.genome_path.read_bytes())
+    assert best.num_inputs == 2 and best.max_nodes == cfg.max_nodes
+    half = run_experiment(cfg.with_overrides(generation_limit=3), tmp_path / "half")
+    st = load_checkpoint(half.checkpoint_path)
+    st.config = cfg
+    save_checkpoint(tmp_path / "half" / "checkpoint.pkl", st)
+    resumed = run_experiment(None, tmp_path / "resumed", resume_path=tmp_path / "half" / "checkpoint.pkl")
+    assert resumed.stats_path.read_text() == full.stats_path.read_text()
+    assert resumed.genome_path.read_bytes() == full.genome_path.read_bytes()
+
+
+def test_run_bench_csv(tn, tmp_path):
+    """bench.csv keeps the reference columns (filled by timing the reference
+    module, the checker) and adds the GPU path's per-generation seconds."""
+    import os
+    import sys
+    from conftest import REPO
+    from paper_2404_01817_b200.runner import BENCH_HEADER, run_bench
+    ref_dir = os.path.join(REPO, "oracle", "_ref")
+    reference = None
+    if os.path.isdir(os.path.join(ref_dir, "arrayneat")):
+        sys.path.insert(0, ref_dir)
+        import arrayneat as reference
+    cfg = tn.NeatConfig(seed=1, pop_size=40)
+    path = run_bench(cfg, [40, 60], 2, tmp_path, reference=reference)
+    lines = path.read_text().splitlines()
+    assert lines[0] == BENCH_HEADER and len(lines) == 5
+    for ln in lines[1:]:
+        cells = ln.split(",")
+        assert float(cells[4]) > 0
+        if reference is not None:
+            assert float(cells[2]) > 0 and float(cells[3]) > 0
