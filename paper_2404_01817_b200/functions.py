@@ -12,6 +12,8 @@ ones raises ``ConfigError`` instead of silently computing something else.
 
 from __future__ import annotations
 
+import sys
+
 from .errors import ConfigError
 
 ACTIVATION_NAMES = {0: "identity", 1: "tanh", 2: "sigmoid", 3: "relu"}
@@ -64,9 +66,22 @@ def check_registry(registry) -> None:
     if isinstance(registry, FunctionRegistry):
         registry.check_builtin()
         return
-    # a reference arrayneat.FunctionRegistry: compare names code by code
+    # a reference arrayneat.FunctionRegistry: compare names code by code, and
+    # the callables against the built-in tables of the registry's own module
+    # (a custom function registered under a built-in name is still custom)
     acts = getattr(registry, "activations", None)
     aggs = getattr(registry, "aggregations", None)
     if acts is None or aggs is None:
         raise ConfigError("registry must provide activations/aggregations tables")
     FunctionRegistry(acts, aggs).check_builtin()
+    mod = sys.modules.get(type(registry).__module__)
+    for table, base_name, kind in ((acts, "ACTIVATIONS", "activation"), (aggs, "AGGREGATIONS", "aggregation")):
+        base = getattr(mod, base_name, None)
+        if not isinstance(base, dict):
+            continue
+        for code, entry in table.items():
+            fn = entry[1] if isinstance(entry, tuple) and len(entry) > 1 else None
+            ref = base.get(int(code))
+            if fn is not None and ref is not None and fn is not ref[1]:
+                raise ConfigError(f"{kind} code {code} ({entry[0]!r}) is a custom callable; only the built-in "
+                                  "functions are compiled into the device kernels")

@@ -145,3 +145,21 @@ def test_checkpoint_interchangeable_with_reference(ref, corpus, tmp_path):
     assert np.array_equal(back.species[2].member_indices, np.arange(2, 200, 3))
     assert back.species[1].best_fitness_history == [0.1, 0.2]
     assert back.config == state.config
+
+
+def test_custom_registry_rejected_clearly(ref):
+    """SURVEY.md §8f.4: user callables cannot run in the kernels -> ConfigError;
+    the reference's default registry is accepted."""
+    import numpy as np
+    from paper_2404_01817_b200 import ConfigError
+    from paper_2404_01817_b200.functions import check_registry
+    check_registry(ref.DEFAULT_REGISTRY)
+    check_registry(ref.FunctionRegistry())
+    custom = dict(ref.FunctionRegistry().activations)
+    custom[1] = ("tanh", lambda x: np.tanh(2 * x))  # built-in name, custom function
+    with pytest.raises(ConfigError):
+        check_registry(ref.FunctionRegistry(activations=custom))
+    extra = dict(ref.FunctionRegistry().activations)
+    extra[7] = ("softsign", lambda x: x / (1 + abs(x)))
+    with pytest.raises(ConfigError):
+        check_registry(ref.FunctionRegistry(activations=extra))
