@@ -106,6 +106,17 @@ __device__ __forceinline__ void load_u32(const uint32_t* p, uint32_t (&out)[N]) 
   }
 }
 
+// the first two rounds' program words of a group (<= 8 entries for GW <= 4),
+// loaded one group ahead by the sweep loop
+struct Words {
+  uint32_t o[8];
+  float w[8];
+};
+__device__ __forceinline__ void load_words(Words& d, const uint32_t* off_s, const float* w_s, int e) {
+  load_u32<8>(off_s + e, d.o);
+  load_f32<8>(w_s + e, d.w);
+}
+
 // two rounds of a sum group: 2*GW value loads (byte offsets into the thread's
 // value column), then one FFMA2 (or FFMA for S = 1) per edge and sample pair
 template <int S, int G, int GW>
@@ -147,7 +158,8 @@ __device__ __forceinline__ void sum_rounds(float2 (&acc)[G][(S + 1) / 2], const 
 template <int S, int G, int RB, bool TANH>
 __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t* __restrict__ off_s,
                                               const float* __restrict__ w_s,
-                                              const StepT<float>* __restrict__ st, char* vb) {
+                                              const StepT<float>* __restrict__ st, char* vb,
+                                              const Words* pre = nullptr) {
   constexpr int GW = G == 3 ? 4 : G;
   constexpr int SP = (S + 1) / 2;  // sample pairs: Blackwell packed fp32 (FFMA2 / FADD2)
   using PackT = Pack<float, S>;
@@ -156,12 +168,28 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
   for (int j = 0; j < G; ++j)
 #pragma unroll
     for (int p = 0; p < SP; ++p) acc[j][p] = make_float2(0.0f, 0.0f);
+  // step records are read up front so the epilogue does not wait on them
+  uint32_t slot_j[G];
+  float rk_j[G], bk_j[G];
+  if constexpr (TANH) {
+    constexpr float K = -2.8853900817779268f;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const StepT<float> sj = st[j];
+      slot_j[j] = sj.slot;
+      rk_j[j] = sj.resp * K;
+      bk_j[j] = sj.bias * K;
+    }
+  }
   const uint32_t* op = off_s + gr.e_begin;
   const float* wp = w_s + gr.e_begin;
   const int rounds = gr.rounds;  // even; holes read the zero slot with weight 0
   uint32_t oa[2 * GW], ob[2 * GW];
   float wa[2 * GW], wb[2 * GW];
-  if (rounds > 0) {
+  if (pre) {
+#pragma unroll
+    for (int q = 0; q < 2 * GW; ++q) { oa[q] = pre->o[q]; wa[q] = pre->w[q]; }
+  } else if (rounds > 0) {
     load_u32<2 * GW>(op, oa);
     load_f32<2 * GW>(wp, wa);
   }
@@ -178,11 +206,9 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
   if constexpr (TANH) {
     // tanh(b + r*a) = 2 / (1 + 2^(k (b + r*a))) - 1, k = -2 log2(e): one FFMA into
     // EX2 (k folded into b and r once per step), FADD, RCP, FFMA -- |err| <~ 2e-7
-    constexpr float K = -2.8853900817779268f;
 #pragma unroll
     for (int j = 0; j < G; ++j) {
-      const StepT<float> sj = st[j];
-      const float rk = sj.resp * K, bk = sj.bias * K;
+      const float rk = rk_j[j], bk = bk_j[j];
       PackT y;
       if constexpr (S == 1) {
         y.v[0] = fmaf(2.0f, rcp_approx(1.0f + ex2_approx(fmaf(rk, acc[j][0].x, bk))), -1.0f);
@@ -201,7 +227,7 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
           y.v[2 * p + 1] = yy.y;
         }
       }
-      if (sj.slot != NO_SLOT) *reinterpret_cast<PackT*>(vb + sj.slot * RB) = y;
+      if (slot_j[j] != NO_SLOT) *reinterpret_cast<PackT*>(vb + slot_j[j] * RB) = y;
     }
   } else {
 #pragma unroll
@@ -269,22 +295,23 @@ __device__ __forceinline__ void run_generic_step(const GroupRec& gr, const uint3
 
 template <typename T, int S, int RB>
 __device__ __forceinline__ void run_group(const GroupRec& gr, const uint32_t* src_s, const float* w_s,
-                                          const EdgeD* ed_s, const StepT<T>* st, char* vb) {
+                                          const EdgeD* ed_s, const StepT<T>* st, char* vb,
+                                          const Words* pre = nullptr) {
   if (!(gr.cls & GRP_GENERIC)) {
     if constexpr (sizeof(T) == 4) {
       if (gr.cls & GRP_TANH_SUM) {
         switch (gr.n) {
-          case 1: run_sum_group<S, 1, RB, true>(gr, src_s, w_s, st, vb); break;
-          case 2: run_sum_group<S, 2, RB, true>(gr, src_s, w_s, st, vb); break;
-          case 3: run_sum_group<S, 3, RB, true>(gr, src_s, w_s, st, vb); break;
-          default: run_sum_group<S, 4, RB, true>(gr, src_s, w_s, st, vb); break;
+          case 1: run_sum_group<S, 1, RB, true>(gr, src_s, w_s, st, vb, pre); break;
+          case 2: run_sum_group<S, 2, RB, true>(gr, src_s, w_s, st, vb, pre); break;
+          case 3: run_sum_group<S, 3, RB, true>(gr, src_s, w_s, st, vb, pre); break;
+          default: run_sum_group<S, 4, RB, true>(gr, src_s, w_s, st, vb, pre); break;
         }
       } else {
         switch (gr.n) {
-          case 1: run_sum_group<S, 1, RB, false>(gr, src_s, w_s, st, vb); break;
-          case 2: run_sum_group<S, 2, RB, false>(gr, src_s, w_s, st, vb); break;
-          case 3: run_sum_group<S, 3, RB, false>(gr, src_s, w_s, st, vb); break;
-          default: run_sum_group<S, 4, RB, false>(gr, src_s, w_s, st, vb); break;
+          case 1: run_sum_group<S, 1, RB, false>(gr, src_s, w_s, st, vb, pre); break;
+          case 2: run_sum_group<S, 2, RB, false>(gr, src_s, w_s, st, vb, pre); break;
+          case 3: run_sum_group<S, 3, RB, false>(gr, src_s, w_s, st, vb, pre); break;
+          default: run_sum_group<S, 4, RB, false>(gr, src_s, w_s, st, vb, pre); break;
         }
       }
     } else {
@@ -407,7 +434,11 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
       const int t1 = t0 + TT;
       prefetch_l2(gin + (int64_t)t1 * I, (uint32_t)(min(TT, B - t1) * I * 4));
     }
+#ifdef TNEAT_DIAG_NOSTAGE  // diagnostic builds only: sweep over stale inputs
+    if (tile == run * tpc && vec_in && cps_shift >= 0) {
+#else
     if (vec_in && cps_shift >= 0) {  // I/4 chunks per input row is a power of two
+#endif
       const float4* src = reinterpret_cast<const float4*>(gin + (int64_t)t0 * I);
       const int n4 = nt * I / 4;
       for (int c = tid; c < n4; c += NT) {
@@ -439,9 +470,25 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
     const int s0 = t0 + tid * S;
 
     // node sweep, one group of independent same-level nodes at a time
+#ifdef TNEAT_DIAG_NOSWEEP  // diagnostic builds only: staging and outputs alone
+    if (n_groups < 0)
+#endif
+    // the next group's record is loaded while this group runs (look-ahead past
+    // the last record reads the step table: still shared memory)
+    // (two records ahead), and -- fp32 -- the next group's first program words
+    uint4 raw_next = reinterpret_cast<const uint4*>(gr_s)[0];
+    uint4 raw_next2 = reinterpret_cast<const uint4*>(gr_s)[1];
+    Words cur, nxt;
+    if constexpr (sizeof(T) == 4) {
+      if (n_groups > 0) load_words(cur, src_s, w_s, (int)(raw_next.y & 0xFFFF));
+    }
 #pragma unroll 1
     for (int g = 0; g < n_groups; ++g) {
-      const uint4 raw = reinterpret_cast<const uint4*>(gr_s)[g];  // one LDS.128
+      const uint4 raw = raw_next;
+      raw_next = raw_next2;
+      raw_next2 = reinterpret_cast<const uint4*>(gr_s)[g + 2];
+      if constexpr (sizeof(T) == 4)
+        load_words(nxt, src_s, w_s, g + 1 < n_groups ? (int)(raw_next.y & 0xFFFF) : 0);
       GroupRec gr;
       gr.n = (uint8_t)(raw.x & 0xFF);
       gr.cls = (uint8_t)((raw.x >> 8) & 0xFF);
@@ -452,7 +499,8 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
       gr.cnt[1] = (uint16_t)(raw.z >> 16);
       gr.cnt[2] = (uint16_t)(raw.w & 0xFFFF);
       gr.cnt[3] = (uint16_t)(raw.w >> 16);
-      run_group<T, S, RB>(gr, src_s, w_s, ed_s, st_s + gr.step_begin, vb);
+      run_group<T, S, RB>(gr, src_s, w_s, ed_s, st_s + gr.step_begin, vb, sizeof(T) == 4 ? &cur : nullptr);
+      if constexpr (sizeof(T) == 4) cur = nxt;
     }
 
     // outputs (P, B, O): one S-wide load per output slot, 16-byte stores per input
@@ -564,6 +612,19 @@ __device__ __forceinline__ void run_split_group(const GroupSplit& gr, const uint
   for (int j = 0; j < G; ++j)
 #pragma unroll
     for (int p = 0; p < SP; ++p) acc[j][p] = make_float2(0.0f, 0.0f);
+  // step records are read up front so the epilogue does not wait on them
+  uint32_t slot_j[G];
+  float rk_j[G], bk_j[G];
+  if constexpr (TANH) {
+    constexpr float K = -2.8853900817779268f;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const StepT<float> sj = st[j];
+      slot_j[j] = sj.slot;
+      rk_j[j] = sj.resp * K;
+      bk_j[j] = sj.bias * K;
+    }
+  }
   {  // input block: TMEM columns, two rounds per wait::ld
     const uint32_t* op = off_s + gr.e_in;
     const float* wp = w_s + gr.e_in;
@@ -601,11 +662,9 @@ __device__ __forceinline__ void run_split_group(const GroupSplit& gr, const uint
     }
   }
   if constexpr (TANH) {
-    constexpr float K = -2.8853900817779268f;
 #pragma unroll
     for (int j = 0; j < G; ++j) {
-      const StepT<float> sj = st[j];
-      const float rk = sj.resp * K, bk = sj.bias * K;
+      const float rk = rk_j[j], bk = bk_j[j];
       PackT y;
       if constexpr (S == 1) {
         y.v[0] = fmaf(2.0f, rcp_approx(1.0f + ex2_approx(fmaf(rk, acc[j][0].x, bk))), -1.0f);
@@ -620,7 +679,7 @@ __device__ __forceinline__ void run_split_group(const GroupSplit& gr, const uint
           y.v[2 * p + 1] = yy.y;
         }
       }
-      if (sj.slot != NO_SLOT) *reinterpret_cast<PackT*>(vb + sj.slot * RB) = y;
+      if (slot_j[j] != NO_SLOT) *reinterpret_cast<PackT*>(vb + slot_j[j] * RB) = y;
     }
   } else {
 #pragma unroll
