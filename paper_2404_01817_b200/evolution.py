@@ -287,11 +287,11 @@ def speciate(pop: PopulationTensors, species: list, config: NeatConfig, rng=None
     # takes every unassigned genome within the threshold (exactly the
     # reference's index-order loop, evolution.py:542-559)
     while True:
-        un = torch.nonzero(assigned < 0)
-        if un.numel() == 0:
+        has_free, first_free = (assigned < 0).to(torch.int8).max(dim=0)  # max -> first index of it
+        if not bool(has_free):
             break
         if len(rows) < config.max_species:
-            i = int(un[0, 0])
+            i = int(first_free)
             founder = _genome_host(nd, cd, i, pop.num_inputs, pop.num_outputs)
             d = _distance_dev(nd, cd, nd[i:i + 1], cd[i:i + 1], config, 1)
             rows.append((next_key, None, founder, d))
@@ -305,14 +305,28 @@ def speciate(pop: PopulationTensors, species: list, config: NeatConfig, rng=None
             near = keys[mat.argmin(dim=0)]
             assigned = torch.where(assigned < 0, near, assigned)
             break
-    assigned_h = assigned.cpu().numpy()
+    # representative refresh on the device: members of row r are the genomes
+    # assigned its key; the new representative is the member closest to the
+    # row's old representative, first index on ties (evolution.py:561-573)
+    R = len(rows)
+    keys_d = torch.tensor([r[0] for r in rows], dtype=torch.int64, device=nd.device)
+    rowid = torch.searchsorted(keys_d, assigned)  # row keys are ascending
+    dist = torch.stack([r[3] for r in rows])  # (R, P)
+    mine = torch.arange(R, device=nd.device)[:, None] == rowid[None, :]
+    masked = torch.where(mine, dist, torch.full_like(dist, math.inf))
+    best = masked.min(dim=1, keepdim=True).values
+    hit = mine & (masked == best)
+    closest_d = hit.to(torch.int8).argmax(dim=1)  # first index reaching the minimum
+    order = torch.argsort(rowid, stable=True)  # members grouped by row, ascending index
+    counts = torch.bincount(rowid, minlength=R)
+    assigned_h, order_h, counts_h, closest_h = (t.cpu().numpy() for t in (assigned, order, counts, closest_d))
+    starts = np.concatenate([[0], np.cumsum(counts_h)])
     result = []
-    for key, previous, rep, drow in rows:
-        members = np.nonzero(assigned_h == key)[0]
+    for k, (key, previous, rep, drow) in enumerate(rows):
+        members = order_h[starts[k]:starts[k + 1]]
         if members.size == 0:
             continue
-        dm = drow.cpu().numpy()[members]
-        closest = int(members[int(np.argmin(dm))])
+        closest = int(closest_h[k])
         new_rep = _genome_host(nd, cd, closest, pop.num_inputs, pop.num_outputs)
         if previous is not None:
             result.append(replace(previous, representative=new_rep, member_indices=members, spawn_count=0))
@@ -370,6 +384,21 @@ def allocate_spawns(species: list, fitness, config: NeatConfig) -> list:
 # reproduction and the generation step
 # ---------------------------------------------------------------------------
 
+def _ranked_head(m: np.ndarray, fit: np.ndarray, k: int) -> np.ndarray:
+    """First k of ``m[lexsort((m, -fit[m]))]`` (fitness descending, index
+    ascending on ties; NaN last) without sorting the whole species: an O(n)
+    partition picks the candidates at or above the k-th value, then only
+    those are sorted."""
+    if k >= m.size or m.size < 4096:
+        return m[np.lexsort((m, -fit[m]))][:k]
+    neg = -fit[m]
+    kth = np.partition(neg, k - 1)[k - 1]
+    if np.isnan(kth):
+        return m[np.lexsort((m, neg))][:k]
+    cand = m[neg <= kth]
+    return cand[np.lexsort((cand, -fit[cand]))][:k]
+
+
 def slot_tables(species: list, fitness, config: NeatConfig):
     """Deterministic slot layout (evolution.py:659-679): species in key order,
     elites first; parent pool = top ceil(survival * n) by (-fitness, index)."""
@@ -382,11 +411,12 @@ def slot_tables(species: list, fitness, config: NeatConfig):
     slot, pooled = 0, 0
     for sp in sorted(species, key=lambda s: s.species_key):
         m = np.asarray(sp.member_indices)
-        ranking = m[np.lexsort((m, -fit[m]))]
         spawn = sp.spawn_count
-        n_el = min(config.genome_elitism, spawn, ranking.size)
+        n_surv = max(1, math.ceil(config.survival_threshold * m.size))
+        n_el = min(config.genome_elitism, spawn, m.size)
+        ranking = _ranked_head(m, fit, max(n_surv, n_el))
         elite[slot:slot + n_el] = ranking[:n_el]
-        surv = ranking[:max(1, math.ceil(config.survival_threshold * ranking.size))]
+        surv = ranking[:n_surv]
         off[slot + n_el:slot + spawn] = pooled
         size[slot + n_el:slot + spawn] = surv.size
         pools.append(surv)
