@@ -292,9 +292,8 @@ def speciate(pop: PopulationTensors, species: list, config: NeatConfig, rng=None
             break
         if len(rows) < config.max_species:
             i = int(first_free)
-            founder = _genome_host(nd, cd, i, pop.num_inputs, pop.num_outputs)
             d = _distance_dev(nd, cd, nd[i:i + 1], cd[i:i + 1], config, 1)
-            rows.append((next_key, None, founder, d))
+            rows.append((next_key, None, None, d))  # representative: refreshed below
             take = (assigned < 0) & (d <= thr)
             take[i] = True
             assigned = torch.where(take, torch.full_like(assigned, next_key), assigned)
@@ -319,15 +318,19 @@ def speciate(pop: PopulationTensors, species: list, config: NeatConfig, rng=None
     closest_d = hit.to(torch.int8).argmax(dim=1)  # first index reaching the minimum
     order = torch.argsort(rowid, stable=True)  # members grouped by row, ascending index
     counts = torch.bincount(rowid, minlength=R)
-    assigned_h, order_h, counts_h, closest_h = (t.cpu().numpy() for t in (assigned, order, counts, closest_d))
+    # one device->host copy for the assignment, grouping and new representatives
+    packed = torch.cat([assigned, order, counts, closest_d]).cpu().numpy()
+    assigned_h, order_h = packed[:count], packed[count:2 * count]
+    counts_h, closest_h = packed[2 * count:2 * count + R], packed[2 * count + R:]
+    reps_n = nd.index_select(0, closest_d).cpu().numpy()
+    reps_c = cd.index_select(0, closest_d).cpu().numpy()
     starts = np.concatenate([[0], np.cumsum(counts_h)])
     result = []
     for k, (key, previous, rep, drow) in enumerate(rows):
         members = order_h[starts[k]:starts[k + 1]]
         if members.size == 0:
             continue
-        closest = int(closest_h[k])
-        new_rep = _genome_host(nd, cd, closest, pop.num_inputs, pop.num_outputs)
+        new_rep = GenomeTensors(reps_n[k].copy(), reps_c[k].copy(), pop.num_inputs, pop.num_outputs)
         if previous is not None:
             result.append(replace(previous, representative=new_rep, member_indices=members, spawn_count=0))
         else:

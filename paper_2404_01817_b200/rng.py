@@ -38,7 +38,13 @@ def _absorb(keys: np.ndarray, tokens: np.ndarray) -> np.ndarray:
 
 
 def mix64_int(z: int) -> int:
-    return int(_mix(np.array([z & M64], dtype=np.uint64))[0])
+    """splitmix64 finaliser on a Python int (same bits as ``_mix``)."""
+    z &= M64
+    z ^= z >> 30
+    z = (z * 0xBF58476D1CE4E5B9) & M64
+    z ^= z >> 27
+    z = (z * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
 
 
 def key_of(seed: int, *path: int) -> int:
@@ -71,7 +77,19 @@ class RngStream:
         self._counter = 0
 
     def child(self, *tokens: int) -> "RngStream":
-        return RngStream(self.master_seed, self.path + tuple(int(t) for t in tokens))
+        toks = tuple(int(t) for t in tokens)
+        if self.batch_shape != ():
+            return RngStream(self.master_seed, self.path + toks)
+        # scalar stream: absorb the new tokens into this key (no re-derivation
+        # of the whole path; same bits as __init__)
+        k = int(self._keys.reshape(-1)[0])
+        for t in toks:
+            k = mix64_int(k ^ mix64_int((t & M64) + GOLDEN))
+        out = RngStream.__new__(RngStream)
+        out.master_seed, out.path, out.batch_shape = self.master_seed, self.path + toks, ()
+        out._keys = np.array([k], dtype=np.uint64)
+        out._counter = 0
+        return out
 
     def split(self, tokens) -> "RngStream":
         tokens = np.asarray(tokens, dtype=np.int64)
