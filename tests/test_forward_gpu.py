@@ -196,3 +196,22 @@ def test_single_genome_wrappers(tn):
         tn.forward(t, None, [1.0, np.nan])
     with pytest.raises(tn.InvalidInput):
         tn.forward(t, None, [1.0, 2.0, 3.0])
+
+
+def test_host_pipeline_matches_device(tn):
+    """The end-to-end host path (pinned host tensors, chunked H2D / kernel /
+    D2H on three streams) returns exactly the device-resident result, for
+    several chunk sizes and both public entry points."""
+    import torch
+    from oracle.arrayneat_oracle import synthetic_population
+    from paper_2404_01817_b200.inference import _host_forward_pipelined
+    nodes, conns = synthetic_population(37, 128, 512, 32, 8, seed=81)
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8)
+    x = torch.randn(37, 700, 32, generator=torch.Generator().manual_seed(4)).pin_memory()
+    ref = tn.forward_device(st, x.cuda()).cpu()
+    for chunk in (1 << 20, 3 << 20, 1 << 30):
+        out = torch.empty((37, 700, 8), dtype=torch.float32).pin_memory()
+        got = _host_forward_pipelined(st, x, out, chunk_bytes=chunk)
+        assert torch.equal(got, ref), chunk
+    assert torch.equal(tn.forward_arrays(st, None, x), ref)
+    np.testing.assert_array_equal(tn.forward_arrays(st, None, x.numpy()), ref.numpy().astype(np.float64))
