@@ -214,6 +214,11 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
         packed = (ki << 16) | (uint64_t)r;
         f = F_LIVE | (ki < (uint64_t)I ? F_INPUT : 0) | (ki >= (uint64_t)I && ki < (uint64_t)io ? F_OUTPUT : 0);
         ++n_live;
+        if (ki >= (uint64_t)I) {  // the reference evaluates every live non-input node (pruned ones too)
+          const double av = gn[(int64_t)r * 5 + 4], gv = gn[(int64_t)r * 5 + 3];
+          if (!(av >= 0.0 && av < ACT_COUNT && av == floor(av))) status |= ST_BAD_ACT;
+          if (!(gv >= 0.0 && gv < AGG_COUNT && gv == floor(gv))) status |= ST_BAD_AGG;
+        }
       }
       s.flags[r] = f;
       s.needed[r] = 0;

@@ -263,10 +263,75 @@ def _genome_host(nodes, conns, i: int, n_in: int, n_out: int) -> GenomeTensors:
     return GenomeTensors(np.array(n, copy=True), np.array(c, copy=True), n_in, n_out)
 
 
+# populations up to this size run the speciation bookkeeping on the host (one
+# read-back of the distance rows; launch latency dominates small populations);
+# larger ones keep it on the device
+SMALL_SPECIATE = 8192
+
+
+def _speciate_host(pop, nd, cd, ordered: list, config: NeatConfig):
+    """speciate() for small populations: device distance rows, host bookkeeping
+    (same decisions as the device path and the reference loop)."""
+    count = int(nd.shape[0])
+    thr = float(config.compatibility_threshold)
+    rows = []  # (key, previous state or None, distance row (P,) host)
+    assigned = np.full(count, -1, dtype=np.int64)
+    if ordered:
+        rn = _dev64(np.stack([sp.representative.nodes for sp in ordered]))
+        rc = _dev64(np.stack([sp.representative.conns for sp in ordered]))
+        mat = _distance_dev(nd, cd, rn, rc, config, 0).cpu().numpy().reshape(len(ordered), count)
+        rows = [(sp.species_key, sp, mat[k]) for k, sp in enumerate(ordered)]
+        ok = mat <= thr
+        keys = np.array([sp.species_key for sp in ordered], dtype=np.int64)
+        assigned = np.where(ok.any(axis=0), keys[ok.argmax(axis=0)], assigned)
+    next_key = max((r[0] for r in rows), default=-1) + 1
+    while True:
+        free = np.flatnonzero(assigned < 0)
+        if free.size == 0:
+            break
+        if len(rows) < config.max_species:
+            i = int(free[0])
+            d = _distance_dev(nd, cd, nd[i:i + 1], cd[i:i + 1], config, 1).cpu().numpy().reshape(count)
+            rows.append((next_key, None, d))
+            take = (assigned < 0) & (d <= thr)
+            take[i] = True
+            assigned[take] = next_key
+            next_key += 1
+        else:
+            keys = np.array([r[0] for r in rows], dtype=np.int64)
+            near = keys[np.stack([r[2] for r in rows]).argmin(axis=0)]
+            assigned = np.where(assigned < 0, near, assigned)
+            break
+    members, closest = [], []
+    for key, _, d in rows:
+        m = np.flatnonzero(assigned == key)
+        members.append(m)
+        closest.append(int(m[int(np.argmin(d[m]))]) if m.size else 0)
+    return rows, assigned, members, closest
+
+
 def speciate(pop: PopulationTensors, species: list, config: NeatConfig, rng=None, sequential: bool = False):
     """Assign species and refresh representatives (evolution.py:513-576)."""
     nd, cd = _dev64(pop.nodes), _dev64(pop.conns)
     count = int(nd.shape[0])
+    if count <= SMALL_SPECIATE:
+        ordered = sorted(species, key=lambda sp: sp.species_key)
+        rows, assigned_h, members_l, closest = _speciate_host(pop, nd, cd, ordered, config)
+        idx = torch.tensor(closest, dtype=torch.int64, device=nd.device)
+        reps_n = nd.index_select(0, idx).cpu().numpy()
+        reps_c = cd.index_select(0, idx).cpu().numpy()
+        result = []
+        for k, (key, previous, _) in enumerate(rows):
+            if members_l[k].size == 0:
+                continue
+            new_rep = GenomeTensors(reps_n[k].copy(), reps_c[k].copy(), pop.num_inputs, pop.num_outputs)
+            if previous is not None:
+                result.append(replace(previous, representative=new_rep, member_indices=members_l[k],
+                                      spawn_count=0))
+            else:
+                result.append(SpeciesState(species_key=key, representative=new_rep, member_indices=members_l[k]))
+        return PopulationTensors(pop.nodes, pop.conns, assigned_h.astype(np.int64), pop.fitness,
+                                 pop.num_inputs, pop.num_outputs), result
     thr = float(config.compatibility_threshold)
     ordered = sorted(species, key=lambda s: s.species_key)
     rows: list = []  # (key, previous state or None, representative, distance row (P,) on device)

@@ -239,13 +239,18 @@ def finalize_transform(stacked: StackedNetworks) -> np.ndarray:
         stacked.maxdims = tuple(int(v) for v in host[:3])
         stacked._cache["status"] = host[3:3 + p]
         stacked._cache["slots"] = host[3 + p:]
-    st = stacked.status
+    return status_cyclic(stacked.status, stacked.mode)
+
+
+def status_cyclic(st: np.ndarray, mode: int = 0) -> np.ndarray:
+    """Raise IntegrityError on structurally invalid genomes (per-genome status
+    bits of the transform); return the cyclic genome indices (feed-forward)."""
     hard = st & (ST_BAD_KEY | ST_DANGLING | ST_MISSING_IO)
     if hard.any():
         bad = np.nonzero(hard)[0]
         raise IntegrityError(f"genome tensors violate structural invariants at indices {bad[:20].tolist()} "
                              f"(status bits {sorted(set(int(x) for x in st[bad[:20]]))})")
-    if stacked.mode == 1:
+    if mode == 1:
         return np.zeros(0, dtype=np.int64)
     return np.nonzero(st & ST_CYCLIC)[0].astype(np.int64)
 
@@ -288,7 +293,10 @@ def transform_population_stacked(pop, **kw) -> StackedNetworks:
 # ---------------------------------------------------------------------------
 
 def _check_codes(stacked: StackedNetworks) -> None:
-    st = stacked.status
+    _check_status_codes(stacked.status)
+
+
+def _check_status_codes(st: np.ndarray) -> None:
     if (st & ~ST_CYCLIC & (ST_BAD_ACT | ST_BAD_AGG)).any():
         which = np.nonzero(st & (ST_BAD_ACT | ST_BAD_AGG))[0][:10].tolist()
         kind = "activation" if (st & ST_BAD_ACT).any() else "aggregation"

@@ -24,8 +24,8 @@ from .config import NeatConfig
 from .device import device, ptr, stream_handle
 from .errors import ConfigError, CycleDetected, ShapeMismatch
 from .functions import DEFAULT_REGISTRY, check_registry
-from .inference import (StackedNetworks, _check_codes, _maxdims_arg, _raise_cycles,
-                        finalize_transform, transform_arrays)
+from .inference import (StackedNetworks, _check_codes, _check_status_codes, _maxdims_arg, _raise_cycles,
+                        status_cyclic, transform_arrays)
 from .rng import RngStream
 
 XOR_INPUTS = np.array([[0.0, 0.0], [0.0, 1.0], [1.0, 0.0], [1.0, 1.0]])
@@ -63,32 +63,78 @@ class Problem:
         """Transform and evaluate the whole population on the device."""
         check_registry(registry)
         rng = rng or RngStream(0)
-        stacked, cyclic = transform_arrays(pop.nodes, pop.conns, pop.num_inputs, pop.num_outputs,
-                                           precision=self.precision, layout="standard")
+        stacked, _ = transform_arrays(pop.nodes, pop.conns, pop.num_inputs, pop.num_outputs,
+                                      precision=self.precision, layout="standard", sync=False)
+        fused = self.fused_launch(stacked)
+        if fused is not None:
+            # one read-back for fitness and per-genome status; the kernel ran
+            # with capacity-sized launch bounds, so no transform read-back first
+            fit, status = fused
+            host = torch.cat([fit, status.to(torch.float64)]).cpu().numpy()
+            self._check(host[stacked.size:].astype(np.int64))
+            return host[:stacked.size]
+        from .inference import finalize_transform
+        cyclic = finalize_transform(stacked)
         if cyclic.size:
             _raise_cycles(cyclic, 0, f"cyclic genomes at indices {cyclic.tolist()}")
         return self.evaluate_stacked(stacked, registry, rng, indices=np.arange(stacked.size))
 
+    def fused_launch(self, stacked: StackedNetworks):
+        """Problems with a fused device fitness return (fitness, status) device
+        tensors without synchronising; others return None."""
+        return None
 
-def _fused(stacked: StackedNetworks, inputs: np.ndarray, kind: int, targets: np.ndarray | None) -> np.ndarray:
-    _check_codes(stacked)
+    @staticmethod
+    def _check(status: np.ndarray) -> None:
+        cyclic = status_cyclic(status)
+        if cyclic.size:
+            _raise_cycles(cyclic, 0, f"cyclic genomes at indices {cyclic.tolist()}")
+        _check_status_codes(status)
+
+
+def _device_const(owner, name: str, a: np.ndarray, dt) -> torch.Tensor:
+    """Problem inputs / targets, copied to the device once per owner object."""
+    cache = owner.__dict__.setdefault("_device_constants", {})
+    key = (name, dt, torch.cuda.current_device())
+    t = cache.get(key)
+    if t is None:
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(device(), dt)
+        cache[key] = t
+    return t
+
+
+def _fused_launch(owner, stacked: StackedNetworks, inputs: np.ndarray, kind: int, targets: np.ndarray | None,
+                  maxdims=None) -> torch.Tensor:
     dt = torch.float64 if stacked.precision & 1 else torch.float32
-    dev = device()
-    x = torch.from_numpy(np.ascontiguousarray(inputs)).to(dev, dt)
-    tg = torch.from_numpy(np.ascontiguousarray(targets, dtype=np.float64)).to(dev) if targets is not None else None
-    fit = torch.empty(stacked.size, dtype=torch.float64, device=dev)
+    x = _device_const(owner, "inputs", inputs, dt)
+    tg = _device_const(owner, "targets", targets, torch.float64) if targets is not None else None
+    fit = torch.empty(stacked.size, dtype=torch.float64, device=x.device)
     _native.call("an_forward_fitness", ptr(stacked.program), stacked.stride, stacked.max_nodes,
-                 stacked.max_conns, stacked.precision, _maxdims_arg(stacked), ptr(x), 0, stacked.size,
+                 stacked.max_conns, stacked.precision, _maxdims_arg(stacked, maxdims), ptr(x), 0, stacked.size,
                  int(x.shape[0]), int(x.shape[1]), stacked.num_outputs, kind, ptr(tg), ptr(fit),
                  stream_handle())
-    return fit.cpu().numpy()
+    return fit
+
+
+def _capacity_dims(stacked: StackedNetworks) -> tuple:
+    """Launch bounds valid for every program of this shape (value slots <= N + 3)."""
+    n = stacked.max_nodes
+    return (n + 3, n, 3 * stacked.max_conns + 12 * n + 16)
+
+
+def _fused(owner, stacked: StackedNetworks, inputs: np.ndarray, kind: int, targets: np.ndarray | None) -> np.ndarray:
+    _check_codes(stacked)
+    return _fused_launch(owner, stacked, inputs, kind, targets).cpu().numpy()
 
 
 class XorProblem(Problem):
     name, input_size, output_size = "xor", 2, 1
 
     def evaluate_stacked(self, stacked, registry, rng, indices=None):
-        return _fused(stacked, XOR_INPUTS, 1, None)
+        return _fused(self, stacked, XOR_INPUTS, 1, None)
+
+    def fused_launch(self, stacked):
+        return _fused_launch(self, stacked, XOR_INPUTS, 1, None, _capacity_dims(stacked)), stacked.status_dev
 
 
 class RegressionProblem(Problem):
@@ -101,10 +147,14 @@ class RegressionProblem(Problem):
             raise ConfigError("regression_samples must be >= 2")
         self.target_fn = REGRESSION_TARGETS[target]
         self.xs = regression_grid(samples)
+        self.xs_col = np.ascontiguousarray(self.xs[:, None])
         self.ys = self.target_fn(self.xs)
 
     def evaluate_stacked(self, stacked, registry, rng, indices=None):
-        return _fused(stacked, self.xs[:, None], 2, self.ys)
+        return _fused(self, stacked, self.xs_col, 2, self.ys)
+
+    def fused_launch(self, stacked):
+        return _fused_launch(self, stacked, self.xs_col, 2, self.ys, _capacity_dims(stacked)), stacked.status_dev
 
 
 class CartPoleProblem(Problem):

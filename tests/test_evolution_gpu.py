@@ -119,7 +119,11 @@ def test_distance_bit_exact(tn):
                           c["dist_pair"])
 
 
-def test_speciate_matches_reference(tn):
+@pytest.mark.parametrize("small", [8192, 0], ids=["host-bookkeeping", "device-bookkeeping"])
+def test_speciate_matches_reference(tn, monkeypatch, small):
+    """Both speciation paths (host bookkeeping for small populations, device
+    bookkeeping for large ones) reproduce the reference exactly."""
+    monkeypatch.setattr(tn.evolution, "SMALL_SPECIATE", small)
     g = load_golden("evolution.npz")
     c = load_golden("corpus.npz")
     n, cc = c["nodes"], c["conns"]

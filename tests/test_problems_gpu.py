@@ -140,3 +140,26 @@ def test_run_bench_csv(tn, tmp_path):
         assert float(cells[4]) > 0
         if reference is not None:
             assert float(cells[2]) > 0 and float(cells[3]) > 0
+
+
+def test_fused_fitness_errors(tn):
+    """The fused path checks the transform status after the kernel: cyclic
+    genomes raise CycleDetected with their indices, unknown codes ConfigError,
+    broken structure IntegrityError -- like the reference (problems.py:209-213)."""
+    g = load_golden("forward_small.npz")
+    nodes, conns = g["nodes"].copy(), g["conns"].copy()
+    pop = tn.PopulationTensors(nodes, conns, None, None, 2, 1)
+    with pytest.raises(tn.CycleDetected) as exc:
+        tn.XorProblem().evaluate_population_tensors(pop)
+    assert exc.value.genome_indices == [47]
+    ok = np.setdiff1d(np.arange(nodes.shape[0]), [47])
+    n2, c2 = nodes[ok].copy(), conns[ok].copy()
+    live = np.nonzero(~np.isnan(n2[3, :, 0]))[0]
+    n2[3, live[-1], 4] = 9.0  # unknown activation code
+    with pytest.raises(tn.ConfigError):
+        tn.XorProblem().evaluate_population_tensors(tn.PopulationTensors(n2, c2, None, None, 2, 1))
+    c3 = conns[ok].copy()
+    lc = np.nonzero(~np.isnan(c3[5, :, 0]))[0]
+    c3[5, lc[0], 0] = 4242.0  # dangling endpoint
+    with pytest.raises(tn.IntegrityError):
+        tn.XorProblem().evaluate_population_tensors(tn.PopulationTensors(nodes[ok].copy(), c3, None, None, 2, 1))
