@@ -509,8 +509,12 @@ def reproduce(pop: PopulationTensors, species: list, fitness, config: NeatConfig
     n, c = int(nd.shape[1]), int(cd.shape[1])
     on = torch.empty((total, n, 5), dtype=torch.float64, device=dev)
     oc = torch.empty((total, c, 4), dtype=torch.float64, device=dev)
-    # keep the device copies referenced until the launch is enqueued
-    pool_d, off_d, size_d, elite_d = (torch.from_numpy(a).to(dev) for a in (pool, off, size, elite))
+    # one host->device copy for the four slot tables; the device views stay
+    # referenced until the launch is enqueued
+    tabs = torch.from_numpy(np.concatenate([pool, off, size, elite]).astype(np.int32)).to(dev)
+    npool = pool.size
+    pool_d, off_d = tabs[:npool], tabs[npool:npool + total]
+    size_d, elite_d = tabs[npool + total:npool + 2 * total], tabs[npool + 2 * total:]
     stage_key = int(np.asarray(rng.child(STAGE_REPRODUCE)._keys).reshape(-1)[0])
     params = mutate_params(config, n, c)
     _native.call("an_reproduce", ptr(nd), ptr(cd), ptr(on), ptr(oc), total, 0, ptr(pool_d), ptr(off_d),
@@ -534,14 +538,21 @@ def evolve_step(pop: PopulationTensors, species: list, config: NeatConfig, rng, 
     evaluated = PopulationTensors(pop.nodes, pop.conns, pop.species_id, fitness, pop.num_inputs,
                                   pop.num_outputs)
     nd, cd = _dev64(pop.nodes), _dev64(pop.conns)
-    live_nodes = (~torch.isnan(nd[:, :, 0])).sum(dim=1).cpu().numpy()
-    live_conns = (~torch.isnan(cd[:, :, 0])).sum(dim=1).cpu().numpy()
     best = int(fitness.argmax())
+    # one read-back: live node / connection counts and the best genome
+    n_, c_ = int(nd.shape[1]), int(cd.shape[1])
+    packed = torch.cat([(~torch.isnan(nd[:, :, 0])).sum(dim=1).to(torch.float64),
+                        (~torch.isnan(cd[:, :, 0])).sum(dim=1).to(torch.float64),
+                        nd[best].reshape(-1), cd[best].reshape(-1)]).cpu().numpy()
+    count = nd.shape[0]
+    live_nodes, live_conns = packed[:count], packed[count:2 * count]
+    best_n = packed[2 * count:2 * count + 5 * n_].reshape(n_, 5).copy()
+    best_c = packed[2 * count + 5 * n_:].reshape(c_, 4).copy()
     stats = GenerationStats(best_fitness=float(fitness[best]), mean_fitness=float(fitness.mean()),
                             species_count=len(species), mean_live_nodes=float(live_nodes.mean()),
                             mean_live_conns=float(live_conns.mean()), elapsed_seconds=0.0, best_index=best,
                             solved=False,
-                            best_genome=_genome_host(nd, cd, best, pop.num_inputs, pop.num_outputs))
+                            best_genome=GenomeTensors(best_n, best_c, pop.num_inputs, pop.num_outputs))
     if stats.best_fitness >= config.fitness_target:
         stats.solved = True
         stats.elapsed_seconds = time.perf_counter() - start
