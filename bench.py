@@ -369,6 +369,11 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    # a small, fixed host thread pool per rank for the per-step host work
+    # (launch planning, read-backs): torchrun's OMP_NUM_THREADS=1 starves it and
+    # a pool of every core makes it erratic
+    import torch
+    torch.set_num_threads(max(1, min(8, (os.cpu_count() or 8) // max(1, world))))
     if world > 1:
         import torch
         import torch.distributed as dist
