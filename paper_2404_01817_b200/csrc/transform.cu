@@ -38,7 +38,7 @@ struct WarpSmem {
   int32_t* in_start;  // [N+1]    CSR by destination into ekey
   int32_t* su_start;  // [N+1]    CSR by source into succ
   int32_t* lvl;       // [N]      topological level
-  int32_t* last_grp;  // [N]      last group that reads the node
+  int32_t* last_grp;  // [N+1]    last group that reads the node (level starts during Kahn)
   uint16_t* succ;     // [C]
   uint16_t* order;    // [N]
   uint16_t* slot_of;  // [N]
@@ -75,7 +75,8 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, bool
   // the arrays that are first written after Kahn (gkey, grp, last_grp,
   // step_row, grp_of)
   const int64_t a_union = take(0, 16);
-  const int64_t a_gkey = take(8ll * Npad, 8), a_grp = take((split ? 32ll : 16ll) * N, 16), a_last = take(4ll * N, 4);
+  const int64_t a_gkey = take(8ll * Npad, 8), a_grp = take((split ? 32ll : 16ll) * N, 16);
+  const int64_t a_last = take(4ll * (N + 1), 4);  // also the level starts of the level-synchronous Kahn
   const int64_t a_srow = take(2ll * N, 2), a_grpof = take(2ll * N, 2);
   const int64_t a_ekey2 = a_union;
   o = a_union + (o - a_union > 8ll * (C > 0 ? C : 1) ? o - a_union : 8ll * (C > 0 ? C : 1));
@@ -307,23 +308,70 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     if (lane == 0) s.ready[w] = m;
   }
   __syncwarp();
-  int n_order = 0;
-  for (; n_order < n_live; ++n_order) {
-    const int pick = warp_first_set(s.ready, W);
-    if (pick < 0) break;
-    __syncwarp();
-    if (lane == 0) {
-      s.ready[pick >> 5] &= ~(1u << (pick & 31));
-      s.order[n_order] = (uint16_t)pick;
+  int n_order = 0, n_levels = 0;
+  const bool exact_order = order_out != nullptr;
+  if (exact_order) {
+    // the reference's order: one node per step, smallest ready row first
+    for (; n_order < n_live; ++n_order) {
+      const int pick = warp_first_set(s.ready, W);
+      if (pick < 0) break;
+      __syncwarp();
+      if (lane == 0) {
+        s.ready[pick >> 5] &= ~(1u << (pick & 31));
+        s.order[n_order] = (uint16_t)pick;
+      }
+      __syncwarp();
+      const int nl = s.lvl[pick] + 1;
+      const int e1 = s.su_start[pick + 1];
+      for (int e = s.su_start[pick] + lane; e < e1; e += 32) {
+        const int d = s.succ[e];
+        atomicMax(&s.lvl[d], nl);
+        if (atomicSub(&s.indeg[d], 1) == 1) atomicOr(&s.ready[d >> 5], 1u << (d & 31));
+      }
+      __syncwarp();
     }
-    __syncwarp();
-    const int nl = s.lvl[pick] + 1;
-    const int e1 = s.su_start[pick + 1];
-    for (int e = s.su_start[pick] + lane; e < e1; e += 32) {
-      const int d = s.succ[e];
-      atomicMax(&s.lvl[d], nl);
-      if (atomicSub(&s.indeg[d], 1) == 1) atomicOr(&s.ready[d >> 5], 1u << (d & 31));
+  } else {
+    // programs only need levels and cycle detection: level-synchronous Kahn,
+    // the whole ready set per round (depth rounds instead of one per node).
+    // s.order gets the nodes level by level; level k starts at last_grp[k].
+    for (;;) {
+      int cnt = 0;
+      uint32_t bits = 0;
+      for (int base = 0; base < W; base += 32) {  // compact the ready set into s.order
+        const int w = base + lane;
+        bits = w < W ? s.ready[w] : 0u;
+        const int c = __popc(bits);
+        int x = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, d);
+          if (lane >= d) x += y;
+        }
+        int at = n_order + cnt + x - c;
+        while (bits) {
+          const int b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          s.order[at++] = (uint16_t)(w * 32 + b);
+        }
+        if (w < W) s.ready[w] = 0u;
+        cnt += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (cnt == 0) break;
+      if (lane == 0) s.last_grp[n_levels] = n_order;
+      __syncwarp();
+      for (int i = n_order + lane; i < n_order + cnt; i += 32) {
+        const int u = s.order[i];
+        s.lvl[u] = n_levels;
+        for (int e = s.su_start[u]; e < s.su_start[u + 1]; ++e) {
+          const int d = s.succ[e];
+          if (atomicSub(&s.indeg[d], 1) == 1) atomicOr(&s.ready[d >> 5], 1u << (d & 31));
+        }
+      }
+      __syncwarp();
+      n_order += cnt;
+      ++n_levels;
     }
+    if (lane == 0) s.last_grp[n_levels] = n_order;
     __syncwarp();
   }
   if (n_order < n_live) status |= ST_CYCLIC;
@@ -352,7 +400,24 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   }
 
   // ---- which nodes matter (ancestor cone of the outputs) and which are read ----
-  if (!recurrent && prune) {
+  if (!recurrent && prune && !exact_order) {
+    // levels in descending order; the nodes of one level are independent
+    for (int r = lane; r < N; r += 32)
+      if (s.flags[r] & F_OUTPUT) s.needed[r] = 1;
+    __syncwarp();
+    for (int lv = n_levels - 1; lv >= 1; --lv) {
+      for (int i = s.last_grp[lv] + lane; i < s.last_grp[lv + 1]; i += 32) {
+        const int r = s.order[i];
+        if (!s.needed[r] || (s.flags[r] & F_INPUT)) continue;
+        for (int e = s.in_start[r]; e < s.in_start[r + 1]; ++e) {
+          const int sr = (int)((s.ekey[e] >> 32) & 0xFFFF);
+          s.needed[sr] = 1;
+          s.used[sr] = 1;
+        }
+      }
+      __syncwarp();
+    }
+  } else if (!recurrent && prune) {
     for (int r = lane; r < N; r += 32)
       if (s.flags[r] & F_OUTPUT) s.needed[r] = 1;
     __syncwarp();

@@ -60,7 +60,7 @@ class StackedNetworks:
     num_inputs: int
     num_outputs: int
     program: torch.Tensor            # (P, stride) uint8
-    order_dev: torch.Tensor          # (P, N) int16, -1 padded
+    order_dev: torch.Tensor | None   # (P, N) int16, -1 padded; computed on first use
     conn_rows: torch.Tensor          # (P, C, 2) int16
     io_rows: torch.Tensor            # (P, I+O) int32
     status_dev: torch.Tensor         # (P,) int32
@@ -98,11 +98,27 @@ class StackedNetworks:
             self._cache["nodes"] = self.nodes_dev.cpu().numpy()
         return self._cache["nodes"]
 
+    def order_device(self) -> torch.Tensor:
+        """The reference's Kahn order (P, N) int16 on the device.  Programs do not
+        need it (levels suffice), so it is computed on first use by a transform
+        pass that also emits the order."""
+        if self.order_dev is None:
+            p, n, c = self.size, self.max_nodes, self.max_conns
+            order = torch.empty((p, n), dtype=torch.int16, device=self.program.device)
+            scratch = torch.empty_like(self.program)
+            status = torch.zeros((p,), dtype=torch.int32, device=self.program.device)
+            md = torch.zeros((3,), dtype=torch.int32, device=self.program.device)
+            _native.call("an_transform", ptr(self.nodes_dev), ptr(self.conns_dev), p, n, c, self.num_inputs,
+                         self.num_outputs, self.mode, self.precision, 1, ptr(scratch), self.stride, ptr(order),
+                         None, None, ptr(status), ptr(md), stream_handle())
+            self.order_dev = order
+        return self.order_dev
+
     @property
     def order(self) -> np.ndarray:
         """(P, N) float64 row order, NaN padded (inference.py:125,133)."""
         if "order" not in self._cache:
-            o = self.order_dev.to(torch.float64)
+            o = self.order_device().to(torch.float64)
             o[o < 0] = float("nan")
             self._cache["order"] = o.cpu().numpy()
         return self._cache["order"]
@@ -135,7 +151,8 @@ class StackedNetworks:
     def select(self, idx) -> "StackedNetworks":
         """Row subset (a view on the same device buffers where possible)."""
         return StackedNetworks(self.nodes_dev[idx], self.conns_dev[idx], self.num_inputs,
-                               self.num_outputs, self.program[idx], self.order_dev[idx],
+                               self.num_outputs, self.program[idx],
+                               None if self.order_dev is None else self.order_dev[idx],
                                self.conn_rows[idx], self.io_rows[idx], self.status_dev[idx],
                                self.maxdims, self.precision, self.mode)
 
@@ -145,8 +162,9 @@ class StackedNetworks:
         first = parts[0]
         md = tuple(max(p.maxdims[k] for p in parts) for k in range(3))
         cat = lambda name: torch.cat([getattr(p, name) for p in parts])  # noqa: E731
+        order = None if any(p.order_dev is None for p in parts) else cat("order_dev")
         return cls(cat("nodes_dev"), cat("conns_dev"), first.num_inputs, first.num_outputs,
-                   cat("program"), cat("order_dev"), cat("conn_rows"), cat("io_rows"),
+                   cat("program"), order, cat("conn_rows"), cat("io_rows"),
                    cat("status_dev"), md, first.precision, first.mode)
 
 
@@ -186,7 +204,8 @@ class TransformedNetwork:
 def transform_arrays(nodes, conns, num_inputs: int, num_outputs: int, *,
                      precision: str = "f32", network_type: str = "feedforward",
                      prune: bool = True, stream: torch.cuda.Stream | None = None,
-                     sync: bool = True, layout: str = "auto") -> tuple[StackedNetworks, np.ndarray]:
+                     sync: bool = True, layout: str = "auto",
+                     with_order: bool = False) -> tuple[StackedNetworks, np.ndarray]:
     """Kahn transform of every genome at once (inference.py:82-147).
 
     Returns the stacked programs and the indices of cyclic genomes (their
@@ -211,13 +230,14 @@ def transform_arrays(nodes, conns, num_inputs: int, num_outputs: int, *,
     stride = int(_native.lib().an_program_stride(n, c, num_outputs, prec))
     dev = nd.device
     program = torch.empty((pop, stride), dtype=torch.uint8, device=dev)
-    order = torch.empty((pop, n), dtype=torch.int16, device=dev)
+    order = torch.empty((pop, n), dtype=torch.int16, device=dev) if with_order else None
     conn_rows = torch.empty((pop, c, 2), dtype=torch.int16, device=dev)
     io_rows = torch.empty((pop, num_inputs + num_outputs), dtype=torch.int32, device=dev)
     status = torch.zeros((pop,), dtype=torch.int32, device=dev)
     maxdims = torch.zeros((3,), dtype=torch.int32, device=dev)
     _native.call("an_transform", ptr(nd), ptr(cd), pop, n, c, num_inputs, num_outputs, mode, prec,
-                 int(bool(prune)), ptr(program), stride, ptr(order), ptr(conn_rows), ptr(io_rows),
+                 int(bool(prune)), ptr(program), stride, ptr(order) if order is not None else None,
+                 ptr(conn_rows), ptr(io_rows),
                  ptr(status), ptr(maxdims), stream_handle(stream))
     stacked = StackedNetworks(nd, cd, num_inputs, num_outputs, program, order, conn_rows, io_rows,
                               status, (0, 0, 0), prec, mode)

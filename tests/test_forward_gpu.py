@@ -215,3 +215,19 @@ def test_host_pipeline_matches_device(tn):
         assert torch.equal(got, ref), chunk
     assert torch.equal(tn.forward_arrays(st, None, x), ref)
     np.testing.assert_array_equal(tn.forward_arrays(st, None, x.numpy()), ref.numpy().astype(np.float64))
+
+
+def test_level_synchronous_programs_equal_exact_order_programs(tn):
+    """Programs built from the level-synchronous Kahn (default) and from the
+    reference's one-node-per-step Kahn (with_order=True) evaluate bitwise
+    identically; the lazily computed order equals the eager one."""
+    import torch
+    from oracle.arrayneat_oracle import synthetic_population
+    for variant in ("T", "M"):
+        nodes, conns = synthetic_population(50, 128, 512, 32, 8, seed=82, variant=variant)
+        a, _ = tn.transform_arrays(nodes, conns, 32, 8)
+        b, _ = tn.transform_arrays(nodes, conns, 32, 8, with_order=True)
+        assert a.order_dev is None and b.order_dev is not None
+        x = torch.randn(50, 300, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+        assert torch.equal(tn.forward_device(a, x), tn.forward_device(b, x))
+        assert np.array_equal(a.order, b.order, equal_nan=True)
