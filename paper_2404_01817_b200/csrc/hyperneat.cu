@@ -28,7 +28,8 @@ constexpr int HN_N1 = 64;          // substrate outputs per genome
 constexpr int HN_G = 4;            // genomes per CTA
 constexpr int HN_N = HN_N1 * HN_G; // MMA N
 constexpr int HN_M = 128;          // rows per tile (MMA M)
-constexpr int HN_THREADS = 128;
+constexpr int HN_THREADS = 512;        // 16 warps: warp w reads TMEM lanes 32*(w%4).. of
+constexpr int HN_SETS = HN_THREADS / 128; // genomes (w/4)*HN_G/HN_SETS .. in the epilogue
 
 // K-major, no-swizzle canonical layout (tc.cuh): 16 K-chunks per 8-row block,
 // consecutive 8-row blocks 2048 B apart
@@ -106,20 +107,26 @@ substrate_kernel(const float* __restrict__ W, int64_t P, const float* __restrict
   uint32_t phase[2] = {0u, 0u};
 
   auto epilogue = [&](int tile, int stage) {
-    // thread = tile row; TMEM lane = 32 * (warp % 4) + lane
-    const float tv = target[(int64_t)tile * HN_M + tid];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(stage * HN_N);
+    // tile row = TMEM lane = 32 * (warp % 4) + lane; warp / 4 picks the genome set
+    const int row = (warp & 3) * 32 + lane;
+    const float tv = target[(int64_t)tile * HN_M + row];
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(stage * HN_N);
+    constexpr int GS = HN_G / HN_SETS;
 #pragma unroll
-    for (int g = 0; g < HN_G; ++g) {
+    for (int gg = 0; gg < GS; ++gg) {
+      const int g = (warp >> 2) * GS + gg;
 #pragma unroll 1
-      for (int q = 0; q < HN_N1 / 16; ++q) {
-        uint32_t r[16];
+      for (int q = 0; q < HN_N1 / 16; q += 2) {  // two 16-column loads per wait
+        uint32_t r[16], r2[16];
         TMEM_LD16(taddr + g * HN_N1 + q * 16, r);
+        TMEM_LD16(taddr + g * HN_N1 + (q + 1) * 16, r2);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const float d = tanh_approx(__uint_as_float(r[i])) - tv;
-          acc_err[g] = fmaf(d, d, acc_err[g]);
+          const float d2 = tanh_approx(__uint_as_float(r2[i])) - tv;
+          acc_err[gg] = fmaf(d, d, acc_err[gg]);
+          acc_err[gg] = fmaf(d2, d2, acc_err[gg]);
         }
       }
     }
@@ -158,13 +165,18 @@ substrate_kernel(const float* __restrict__ W, int64_t P, const float* __restrict
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     epilogue(last, stage);
   }
-  // reduce squared errors over the CTA's 128 rows
+  // reduce squared errors over the CTA's 128 rows (each warp holds GS genomes)
+  {
+    constexpr int GS = HN_G / HN_SETS;
+    if (lane < HN_G) sm.part[warp][lane] = 0.f;
+    __syncwarp();
 #pragma unroll
-  for (int g = 0; g < HN_G; ++g) {
-    float v = acc_err[g];
+    for (int gg = 0; gg < GS; ++gg) {
+      float v = acc_err[gg];
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    if (lane == 0) sm.part[warp][g] = v;
+      for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+      if (lane == 0) sm.part[warp][(warp >> 2) * GS + gg] = v;
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
