@@ -467,22 +467,57 @@ def _ranked_head(m: np.ndarray, fit: np.ndarray, k: int) -> np.ndarray:
     return cand[np.lexsort((cand, -fit[cand]))][:k]
 
 
+def _ranked_heads_device(ordered: list, fit: np.ndarray, heads: list) -> list:
+    """For each species (in key order) the first heads[k] members ranked by
+    (fitness descending, index ascending; NaN last): three stable device sorts
+    over the population and one read-back of the heads."""
+    dev = device()
+    count = fit.size
+    rowid = np.full(count, len(ordered), dtype=np.int64)  # genomes of dropped species sort last
+    for k, sp in enumerate(ordered):
+        rowid[np.asarray(sp.member_indices)] = k
+    f = torch.from_numpy(np.ascontiguousarray(fit)).to(dev)
+    nan = torch.isnan(f)
+    key = torch.where(nan, torch.zeros_like(f), -f) + 0.0  # + 0.0: -0.0 -> +0.0, ties as in numpy
+    idx = torch.argsort(key, stable=True)
+    idx = idx[torch.argsort(nan[idx].to(torch.int8), stable=True)]
+    rid = torch.from_numpy(rowid).to(dev)
+    order = idx[torch.argsort(rid[idx], stable=True)]
+    starts = np.concatenate([[0], np.cumsum([np.asarray(sp.member_indices).size for sp in ordered])])
+    parts = [order[int(starts[k]):int(starts[k]) + heads[k]] for k in range(len(ordered))]
+    flat = torch.cat(parts).cpu().numpy() if parts else np.zeros(0, dtype=np.int64)
+    out, at = [], 0
+    for h in heads:
+        out.append(flat[at:at + h])
+        at += h
+    return out
+
+
+# populations above this size rank the parent pools on the device
+SMALL_SLOT_TABLES = 65536
+
+
 def slot_tables(species: list, fitness, config: NeatConfig):
     """Deterministic slot layout (evolution.py:659-679): species in key order,
     elites first; parent pool = top ceil(survival * n) by (-fitness, index)."""
     fit = np.asarray(fitness.cpu().numpy() if isinstance(fitness, torch.Tensor) else fitness)
     total = config.pop_size
+    ordered = sorted(species, key=lambda s: s.species_key)
+    heads = [max(max(1, math.ceil(config.survival_threshold * np.asarray(sp.member_indices).size)),
+                 min(config.genome_elitism, sp.spawn_count, np.asarray(sp.member_indices).size))
+             for sp in ordered]
+    ranked = _ranked_heads_device(ordered, fit, heads) if fit.size > SMALL_SLOT_TABLES else None
     elite = np.full(total, -1, dtype=np.int32)
     off = np.zeros(total, dtype=np.int32)
     size = np.ones(total, dtype=np.int32)
     pools = []
     slot, pooled = 0, 0
-    for sp in sorted(species, key=lambda s: s.species_key):
+    for k, sp in enumerate(ordered):
         m = np.asarray(sp.member_indices)
         spawn = sp.spawn_count
         n_surv = max(1, math.ceil(config.survival_threshold * m.size))
         n_el = min(config.genome_elitism, spawn, m.size)
-        ranking = _ranked_head(m, fit, max(n_surv, n_el))
+        ranking = ranked[k] if ranked is not None else _ranked_head(m, fit, max(n_surv, n_el))
         elite[slot:slot + n_el] = ranking[:n_el]
         surv = ranking[:n_surv]
         off[slot + n_el:slot + spawn] = pooled

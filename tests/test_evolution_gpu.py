@@ -160,3 +160,30 @@ def test_reproduce_matches_reference(tn):
                                  allocator)
     assert allocator.next_key == int(g["rep_next_key"])
     assert_genomes_match(off.nodes, off.conns, g["rep_nodes"], g["rep_conns"])
+
+
+def test_slot_tables_device_ranking_equals_host(tn, monkeypatch):
+    """Large-population slot tables rank parents with device sorts; they equal
+    the host ranking (fitness descending, index ascending, NaN last, -0 == +0),
+    including genomes of species dropped by stagnation."""
+    from paper_2404_01817_b200.evolution import SpeciesState, slot_tables
+    rng = np.random.default_rng(9)
+    p = 5000
+    fit = rng.choice([0.0, -0.0, 1.5, 2.0, np.nan, -np.inf, 3.25], size=p)  # many ties
+    fit = np.where(rng.random(p) < 0.4, rng.normal(size=p).round(1), fit)
+    sp_of = rng.integers(0, 5, p)
+    g = tn.GenomeTensors(np.zeros((4, 5)), np.zeros((2, 4)), 2, 1)
+    species = [SpeciesState(species_key=k, representative=g, member_indices=np.nonzero(sp_of == k)[0],
+                            spawn_count=0) for k in (0, 1, 2, 4)]  # species 3 was dropped
+    cfg = tn.NeatConfig(pop_size=p, survival_threshold=0.3, genome_elitism=2)
+    counts = np.array([s.member_indices.size for s in species], dtype=float)
+    spawn = np.floor(p * counts / counts.sum()).astype(int)
+    spawn[0] += p - spawn.sum()
+    for s, n in zip(species, spawn):
+        s.spawn_count = int(n)
+    monkeypatch.setattr(tn.evolution, "SMALL_SLOT_TABLES", 10 ** 9)
+    host = slot_tables(species, fit, cfg)
+    monkeypatch.setattr(tn.evolution, "SMALL_SLOT_TABLES", 0)
+    dev = slot_tables(species, fit, cfg)
+    for a, b in zip(host, dev):
+        assert np.array_equal(a, b)
