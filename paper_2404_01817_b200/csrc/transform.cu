@@ -287,6 +287,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     s.succ[s.su_start[sr] + atomicAdd(&s.outdeg[sr], 1)] = (uint16_t)dr;
   }
   __syncwarp();
+  int shadowed_any = 0;
   for (int r = lane; r < N; r += 32) {  // insertion sort of each (small) bucket
     const int b0 = s.in_start[r], b1 = s.in_start[r + 1];
     for (int i = b0 + 1; i < b1; ++i) {
@@ -295,8 +296,61 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       while (j >= b0 && s.ekey[j] > x) { s.ekey[j + 1] = s.ekey[j]; --j; }
       s.ekey[j + 1] = x;
     }
-    s.lvl[r] = 0;
+    // repeated enabled (src, dst) pairs: the reference's dense incoming keeps
+    // the last connection row (inference.py:108-112); the earlier ones are
+    // shadowed -- counted here, removed below
+    int kept = 0;
+    for (int i = b0; i < b1; ++i) {
+      const bool shadow = i + 1 < b1 && ((s.ekey[i] ^ s.ekey[i + 1]) >> 32) == 0;
+      if (shadow) {
+        ++shadowed_any;
+        if (conn_rows) conn_rows[(g * C + (int64_t)(s.ekey[i] & 0xFFFFFFFFu)) * 2 + 0] = -1,
+                       conn_rows[(g * C + (int64_t)(s.ekey[i] & 0xFFFFFFFFu)) * 2 + 1] = -1;
+      } else {
+        ++kept;
+      }
+    }
+    s.lvl[r] = kept;
   }
+  shadowed_any = __reduce_add_sync(0xffffffffu, shadowed_any);
+  __syncwarp();
+  if (shadowed_any) {
+    if (N <= 64) {
+      // the reference's Kahn for N <= 64 decrements through successor bitmasks
+      // (one per pair) while the indegree counts every connection: the
+      // destination never becomes ready and the genome reads as cyclic
+      for (int r = lane; r < N; r += 32) s.indeg[r] += (s.in_start[r + 1] - s.in_start[r]) - s.lvl[r];
+    } else {
+      // N > 64: the Kahn decrements per connection (no effect); the programs
+      // see each pair once, with the last row's weight: compact the buckets
+      // new bucket starts in outdeg (free between the CSR fill and the split
+      // input counts), staging in ekey2 (free since the CSR fill)
+      int carry = 0;
+      for (int base = 0; base < N; base += 32) {
+        const int r = base + lane;
+        const int v = r < N ? s.lvl[r] : 0;
+        int x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, d);
+          if (lane >= d) x += y;
+        }
+        if (r < N) s.outdeg[r] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
+      __syncwarp();
+      for (int r = lane; r < N; r += 32) {
+        int at = s.outdeg[r];
+        for (int i = s.in_start[r]; i < s.in_start[r + 1]; ++i)
+          if (!(i + 1 < s.in_start[r + 1] && ((s.ekey[i] ^ s.ekey[i + 1]) >> 32) == 0)) s.ekey2[at++] = s.ekey[i];
+      }
+      __syncwarp();
+      for (int i = lane; i < carry; i += 32) s.ekey[i] = s.ekey2[i];
+      for (int r = lane; r < N; r += 32) s.in_start[r] = s.outdeg[r];
+      if (lane == 0) s.in_start[N] = carry;
+    }
+  }
+  for (int r = lane; r < N; r += 32) s.lvl[r] = 0;
   __syncwarp();
 
   // ---- Kahn, smallest ready row first (inference.py:127-141) + levels ---------

@@ -180,6 +180,37 @@ def make_forward_goldens() -> None:
     _save("corpus.npz", **case)
 
 
+def make_duplicate_goldens() -> None:
+    """Repeated (in, out) connection pairs (a "collision" the reference does
+    not reject): its dense incoming keeps the last row; with max_nodes <= 64
+    the bitmask Kahn leaves the destination unready (cyclic), above 64 it does
+    not (inference.py:108-141)."""
+    base = np.load(os.path.join(HERE, "forward_small.npz"))
+    nodes, conns = base["nodes"][:12].copy(), base["conns"][:12].copy()
+    rng = np.random.default_rng(31)
+    for p in range(12):
+        live = np.nonzero(~np.isnan(conns[p, :, 0]))[0]
+        free = np.nonzero(np.isnan(conns[p, :, 0]))[0]
+        if live.size == 0 or free.size < 2:
+            continue
+        src = live[int(rng.integers(live.size))]
+        kind = p % 4
+        conns[p, free[0]] = conns[p, src]
+        conns[p, free[0], 3] = float(rng.normal())
+        if kind == 1:
+            conns[p, free[0], 2] = 0.0      # disabled duplicate
+        elif kind == 2:
+            conns[p, free[1]] = conns[p, src]  # triple
+            conns[p, free[1], 3] = float(rng.normal())
+        elif kind == 3:
+            conns[p, [src, free[0]]] = conns[p, [free[0], src]]  # duplicate in the earlier row
+    inputs = np.random.default_rng(6).standard_normal((12, 5, 2))
+    _save("forward_dupes_n12.npz", **_transform_forward_case(nodes, conns, inputs, 2, 1))
+    wide = np.full((12, 80, 5), np.nan)
+    wide[:, :nodes.shape[1]] = nodes
+    _save("forward_dupes_n80.npz", **_transform_forward_case(wide, conns, inputs, 2, 1))
+
+
 def make_rng_goldens() -> None:
     cases = []
     out = {}
@@ -203,9 +234,11 @@ def make_rng_goldens() -> None:
     _save("rng.npz", **out)
 
 
-if __name__ == "__main__" and "evo" not in sys.argv:
+if __name__ == "__main__" and "evo" not in sys.argv and "dupes" not in sys.argv:
     make_rng_goldens()
     make_forward_goldens()
+if __name__ == "__main__" and ("dupes" in sys.argv or "evo" not in sys.argv):
+    make_duplicate_goldens()
 
 
 # -- evolution operators --------------------------------------------------------

@@ -231,3 +231,19 @@ def test_level_synchronous_programs_equal_exact_order_programs(tn):
         x = torch.randn(50, 300, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
         assert torch.equal(tn.forward_device(a, x), tn.forward_device(b, x))
         assert np.array_equal(a.order, b.order, equal_nan=True)
+
+
+@pytest.mark.parametrize("name", ["forward_dupes_n12.npz", "forward_dupes_n80.npz"])
+def test_duplicate_pairs_match_reference(tn, name):
+    """Repeated (in, out) pairs: last row wins in incoming / the forward, and
+    with max_nodes <= 64 the genome reads as cyclic -- as the reference."""
+    g = load_golden(name)
+    st, cyc = tn.transform_arrays(g["nodes"], g["conns"], 2, 1, precision="f64")
+    assert np.array_equal(cyc, g["cyclic"])
+    assert np.array_equal(st.order, g["order"], equal_nan=True)
+    assert np.array_equal(st.incoming, g["incoming"], equal_nan=True)
+    ok = np.setdiff1d(np.arange(g["nodes"].shape[0]), g["cyclic"])
+    if ok.size:
+        st2, _ = tn.transform_arrays(g["nodes"][ok], g["conns"][ok], 2, 1, precision="f64")
+        out = tn.forward_arrays(st2, None, g["inputs"][ok])
+        np.testing.assert_allclose(out, g["outputs"][ok], rtol=1e-9, atol=1e-9)
