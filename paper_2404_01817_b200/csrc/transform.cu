@@ -813,10 +813,10 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
   if (P < 0 || N < 1 || N > 32767 || C < 0 || I < 1 || O < 1 || I + O > N) return -1;
   if ((split ? edge_capacity_split(N, C) : edge_capacity(N, C)) > 65535) return -1;
   if (split && ((precision & FMT_F64) || mode != 0)) return -1;  // split: fp32 feed-forward only
-  if (!nodes || !program || !maxdims || (C > 0 && !conns)) return -2;
   const ProgLayout L = prog_layout(N, C, O, precision);
   if (program_stride != L.stride) return -3;
-  if (P == 0) return 0;
+  if (P == 0) return 0;  // empty population: nothing to read or write
+  if (!nodes || !program || !maxdims || (C > 0 && !conns)) return -2;
   const int Cc = C > 0 ? C : 1;
   const int64_t ws = warp_smem_bytes(N, Cc, split);
   if (ws > 200 * 1024) return -4;  // genome capacity too large for one warp's shared memory

@@ -1,0 +1,91 @@
+"""Edge cases of the transform + forward path against the oracle (pinned to
+the reference by test_oracle_golden.py): empty populations and batches,
+genomes without connections, empty aggregations, unpruned programs, and large
+genome capacities."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import cuda_ok
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tn():
+    if not cuda_ok():
+        pytest.skip("no CUDA device")
+    import paper_2404_01817_b200 as tn
+    return tn
+
+
+def _oracle_out(nodes, conns, x, ni, no):
+    from oracle import arrayneat_oracle as orc
+    return np.stack([orc.forward_genome(nodes[p], orc.transform_genome(nodes[p], conns[p], ni, no), x[p])
+                     for p in range(nodes.shape[0])])
+
+
+def test_empty_population_and_batch(tn):
+    import torch
+    from oracle.arrayneat_oracle import synthetic_population
+    nodes, conns = synthetic_population(3, 64, 128, 4, 2, seed=1, min_conns=10, max_conns_drawn=60)
+    st, _ = tn.transform_arrays(nodes[:0], conns[:0], 4, 2)
+    assert st.size == 0
+    out = tn.forward_device(st, torch.zeros((0, 10, 4), device="cuda"))
+    assert tuple(out.shape) == (0, 10, 2)
+    st, _ = tn.transform_arrays(nodes, conns, 4, 2)
+    out = tn.forward_device(st, torch.zeros((3, 0, 4), device="cuda"))
+    assert tuple(out.shape) == (3, 0, 2)
+    x = np.random.default_rng(0).standard_normal((3, 1, 4))
+    y = tn.forward_arrays(st, None, x.astype(np.float32))
+    np.testing.assert_allclose(y, _oracle_out(nodes, conns, x, 4, 2), rtol=0, atol=1e-5)
+
+
+def test_no_connections_and_empty_aggregations(tn):
+    """Outputs without incoming edges evaluate act(bias + response * 0) for
+    every aggregation (empty aggregation = 0, inference.py:238-240)."""
+    from oracle.arrayneat_oracle import synthetic_population
+    nodes, conns = synthetic_population(8, 32, 64, 3, 4, seed=2, variant="M", min_conns=0, max_conns_drawn=20)
+    conns[:4] = np.nan  # genomes 0-3: no connections at all
+    for agg in range(4):  # output nodes of genome 4 + agg: every aggregation with some empty lists
+        nodes[4 + agg, 3:7, 3] = float(agg)
+    x = np.random.default_rng(3).standard_normal((8, 7, 3))
+    st, cyc = tn.transform_arrays(nodes, conns, 3, 4, precision="f64")
+    assert cyc.size == 0
+    np.testing.assert_allclose(tn.forward_arrays(st, None, x), _oracle_out(nodes, conns, x, 3, 4),
+                               rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.parametrize("precision,tol", [("f64", 1e-9), ("f32", 1e-4)])
+def test_unpruned_programs(tn, precision, tol):
+    """prune=False keeps every live node in the program (no ancestor-cone
+    pruning): same outputs."""
+    from oracle.arrayneat_oracle import synthetic_population
+    nodes, conns = synthetic_population(10, 48, 120, 4, 3, seed=4, variant="M", min_conns=20, max_conns_drawn=100)
+    x = np.random.default_rng(5).standard_normal((10, 9, 4))
+    a, _ = tn.transform_arrays(nodes, conns, 4, 3, precision=precision, prune=False)
+    b, _ = tn.transform_arrays(nodes, conns, 4, 3, precision=precision)
+    ref = _oracle_out(nodes, conns, x, 4, 3)
+    inp = x if precision == "f64" else x.astype(np.float32)
+    for st in (a, b):
+        out = tn.forward_arrays(st, None, inp)
+        assert np.max(np.abs(out - ref) / np.maximum(1.0, np.abs(ref))) <= tol
+    assert a.maxdims[1] >= b.maxdims[1]  # unpruned programs have at least as many steps
+
+
+def test_large_genome_capacity(tn):
+    """max_nodes 512 / max_conns 2048 (far beyond the configs): transform and
+    forward stay exact against the oracle in float64."""
+    from oracle.arrayneat_oracle import synthetic_population
+    nodes, conns = synthetic_population(4, 512, 2048, 16, 4, seed=6, min_conns=1200, max_conns_drawn=2000)
+    x = np.random.default_rng(7).standard_normal((4, 300, 16))
+    st, cyc = tn.transform_arrays(nodes, conns, 16, 4, precision="f64")
+    assert cyc.size == 0
+    np.testing.assert_allclose(tn.forward_arrays(st, None, x), _oracle_out(nodes, conns, x, 16, 4),
+                               rtol=1e-9, atol=1e-9)
+    st32, _ = tn.transform_arrays(nodes, conns, 16, 4)
+    out = tn.forward_arrays(st32, None, x.astype(np.float32))
+    ref = _oracle_out(nodes, conns, x, 16, 4)
+    assert np.max(np.abs(out - ref) / np.maximum(1.0, np.abs(ref))) <= 1e-5
