@@ -15,13 +15,14 @@ ap.add_argument("--pop", type=int, default=10000)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--batch", type=int, default=4096)
+ap.add_argument("--layout", default="auto")
 a = ap.parse_args()
 n, c = synthetic_population(a.pop, 128, 512, 32, 8, seed=20261018)
 nodes, conns = torch.from_numpy(n).cuda(), torch.from_numpy(c).cuda()
 x = torch.randn((a.pop, a.batch, 32), device="cuda")
 out = torch.empty((a.pop, a.batch, 8), device="cuda")
 for _ in range(a.steps):
-    st, _ = tn.transform_arrays(nodes, conns, 32, 8)
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8, layout=a.layout)
     tn.forward_device(st, x, out, variant=a.variant)
 torch.cuda.synchronize()
 print("maxdims", st.maxdims)

@@ -14,6 +14,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--pop", type=int, default=10000)
 ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--reps", type=int, default=4)
+ap.add_argument("--layout", default="auto")
 a = ap.parse_args()
 n, c = synthetic_population(a.pop, 128, 512, 32, 8, seed=20261018)
 nodes, conns = torch.from_numpy(n).cuda(), torch.from_numpy(c).cuda()
@@ -22,12 +23,12 @@ out = torch.empty((a.pop, 4096, 8), device="cuda")
 for rep in range(a.reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    st, _ = tn.transform_arrays(nodes, conns, 32, 8, sync=False)
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8, sync=False, layout=a.layout)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     tn.finalize_transform(st)
     t2 = time.perf_counter()
-    v = (a.variant & 0xF) or 5
+    v = (a.variant & 0xF) or (10 if st.precision & 2 else 5)
     plan = tn.inference._bucket_plan(st, v)
     torch.cuda.synchronize()
     t3 = time.perf_counter()
