@@ -23,8 +23,6 @@
 // activated; node = act(bias + response * agg(w * v)); empty aggregation = 0;
 // mean divides by the incoming count; outputs read at the rows of keys I..I+O-1.
 
-#include <cstdlib>
-
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -1131,7 +1129,6 @@ int launch_tile(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, co
   const int64_t prog_bytes = ms * sizeof(GroupRec) + ms * sizeof(StepT<T>) +
                              (sizeof(T) == 8 ? 16 * me : align_up(4 * me, 16) + 4 * me);
   int64_t smem = align_up(prog_bytes, 16) + (int64_t)max(maxdims_host[0], I) * (TT + S) * sizeof(T);
-  if (const char* pad = getenv("TNEAT_EXPERIMENT_SMEM_PAD")) smem += atoll(pad);  // occupancy experiments only
   if (smem > 227 * 1024) return -6;
   cudaFuncSetAttribute(fwd_tile_kernel<T, S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fwd_tile_kernel<T, S, NT><<<(unsigned)grid, NT, smem, st>>>(prog, L, ids, in, in_gstride, B, I, O, runs, tpc,
