@@ -52,10 +52,10 @@ struct ProgHeader {  // 32 bytes
 // with the same aggregation class.  Their edge lists are interleaved
 // round-major with a row width of gw = (n == 3 ? 4 : n) entries -- edge r of
 // step j sits at e_begin + r*gw + j -- so the forward kernel accumulates the n
-// nodes in lock-step as n independent FMA chains.  Sum/mean groups have an
-// even number of rounds; entries past a step's count are holes that read the
-// genome's zero slot (header n_slots - 1, never written) with weight 0, so the
-// rounds run unpredicated.  e_begin is a multiple of 8, so two rounds of
+// nodes in lock-step as n independent FMA chains.  In sum/mean groups the
+// entries past a step's count are holes that read the genome's zero slot
+// (header n_slots - 1, never written) with weight 0, so the rounds run
+// unpredicated.  e_begin is a multiple of 8, so two rounds of
 // sources / weights are single 16-byte loads.  Non-sum aggregations are
 // singleton groups with exact counts.
 struct __align__(16) GroupRec {  // 16 bytes

@@ -145,6 +145,26 @@ __device__ __forceinline__ void sum_rounds(float2 (&acc)[G][(S + 1) / 2], const 
     }
 }
 
+// one round (the first GW entries of a two-round buffer)
+template <int S, int G, int GW>
+__device__ __forceinline__ void sum_round1(float2 (&acc)[G][(S + 1) / 2], const uint32_t (&off)[2 * GW],
+                                           const float (&w)[2 * GW], const char* vb) {
+  using PackT = Pack<float, S>;
+  PackT v[GW];
+#pragma unroll
+  for (int q = 0; q < G; ++q) v[q] = *reinterpret_cast<const PackT*>(vb + off[q]);
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    if constexpr (S == 1) {
+      acc[q][0].x = fmaf(w[q], v[q].v[0], acc[q][0].x);
+    } else {
+#pragma unroll
+      for (int p = 0; p < S / 2; ++p)
+        acc[q][p] = __ffma2_rn(make_float2(w[q], w[q]), make_float2(v[q].v[2 * p], v[q].v[2 * p + 1]), acc[q][p]);
+    }
+  }
+}
+
 // One sum/mean group of G steps (fp32 program): edge block of width GW = G|4,
 // two rounds per step of the pipeline (2*GW byte offsets in <= two 16-byte
 // loads, weights likewise) and up to 2G independent value loads / FMA chains,
@@ -181,7 +201,7 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
   }
   const uint32_t* op = off_s + gr.e_begin;
   const float* wp = w_s + gr.e_begin;
-  const int rounds = gr.rounds;  // even; holes read the zero slot with weight 0
+  const int rounds = gr.rounds;  // holes read the zero slot with weight 0
   uint32_t oa[2 * GW], ob[2 * GW];
   float wa[2 * GW], wb[2 * GW];
   if (pre) {
@@ -191,12 +211,21 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
     load_u32<2 * GW>(op, oa);
     load_f32<2 * GW>(wp, wa);
   }
+  // round pairs from alternating buffers; an odd last round from the first
+  // half of the buffer that holds it
 #pragma unroll 1
-  for (int r = 0; r < rounds; r += 4) {
+  for (int r = 0;; r += 4) {
+    if (r + 2 > rounds) {
+      if (r < rounds) sum_round1<S, G, GW>(acc, oa, wa, vb);
+      break;
+    }
     load_u32<2 * GW>(op + (r + 2) * GW, ob);
     load_f32<2 * GW>(wp + (r + 2) * GW, wb);
     sum_rounds<S, G, GW>(acc, oa, wa, vb);
-    if (r + 2 >= rounds) break;
+    if (r + 4 > rounds) {
+      if (r + 2 < rounds) sum_round1<S, G, GW>(acc, ob, wb, vb);
+      break;
+    }
     load_u32<2 * GW>(op + (r + 4) * GW, oa);
     load_f32<2 * GW>(wp + (r + 4) * GW, wa);
     sum_rounds<S, G, GW>(acc, ob, wb, vb);

@@ -600,8 +600,8 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
         if (ng > 0) e_total = (int)align_up(e_total + group_width(s.grp[ng - 1].n) * s.grp[ng - 1].rounds, 8);
         GroupRec gr;
         memset(&gr, 0, sizeof(gr));
-        // sum/mean groups: even rounds (two per unrolled iteration), holes read the zero slot
-        gr.cls = (uint8_t)cls; gr.rounds = (uint16_t)(cls == 0 ? (cnt + 1) & ~1 : cnt);
+        // holes (shorter lists in a sum/mean group) read the zero slot
+        gr.cls = (uint8_t)cls; gr.rounds = (uint16_t)cnt;
         gr.e_begin = (uint16_t)e_total; gr.step_begin = (uint16_t)k;
         s.grp[ng++] = gr;
         cur_lv = lv; cur_cls = cls; cur_rounds = cnt;
