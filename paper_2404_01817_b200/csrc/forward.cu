@@ -468,9 +468,28 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
 #endif
       const float4* src = reinterpret_cast<const float4*>(gin + (int64_t)t0 * I);
       const int n4 = nt * I / 4;
-      for (int c = tid; c < n4; c += NT) {
-        const float4 x = __ldg(src + c);
-        TNEAT_SCATTER4(c >> cps_shift, (c & cps_mask) << 2, x);
+      if (cps == 8 && (RB / 4) % 32 == 2) {
+        // I = 32 with a row stride of 2 banks: a warp's 32 lanes hold 4 samples x
+        // 8 input chunks; storing component k of every chunk would hit rows
+        // {0,4,..,28}+k, i.e. every bank twice.  Lanes of the upper 4 chunks
+        // store their components in the order 2,0,3,1 (lower: 0,2,1,3), so the
+        // 8 rows of each store have distinct even residues mod 16 and the
+        // store is conflict-free.
+        for (int c = tid; c < n4; c += NT) {
+          const float4 x = __ldg(src + c);
+          const bool hi = (c & 4) != 0;
+          float* base = vf + (c >> 3) + ((c & 7) << 2) * (RB / 4);
+          const int o2 = hi ? 0 : 2 * (RB / 4), o0 = hi ? 2 * (RB / 4) : 0;
+          base[o0] = hi ? x.z : x.x;
+          base[o2] = hi ? x.x : x.z;
+          base[o0 + (RB / 4)] = hi ? x.w : x.y;
+          base[o2 + (RB / 4)] = hi ? x.y : x.w;
+        }
+      } else {
+        for (int c = tid; c < n4; c += NT) {
+          const float4 x = __ldg(src + c);
+          TNEAT_SCATTER4(c >> cps_shift, (c & cps_mask) << 2, x);
+        }
       }
     } else if (vec_in) {
       const float4* src = reinterpret_cast<const float4*>(gin + (int64_t)t0 * I);
