@@ -28,7 +28,9 @@ extern "C" {
 /* ---- programs ------------------------------------------------------------ */
 
 /* Bytes of one genome's compiled program for capacity (N nodes, C conns, O
- * outputs); precision 0 = fp32 program, 1 = fp64 program. */
+ * outputs).  `precision` is the program format: bit 0 = fp64 program (else
+ * fp32), bit 1 = split program (fp32 feed-forward only: input values in
+ * tensor memory, see an_forward variant 10); 0 = the standard fp32 program. */
 int64_t an_program_stride(int N, int C, int O, int precision);
 
 /* Genome transform.  Replaces inference.transform_arrays
@@ -41,7 +43,12 @@ int64_t an_program_stride(int N, int C, int O, int precision);
  *   mode     0 = feed-forward (cyclic genomes flagged), 1 = recurrent
  *   prune    1 = drop nodes outside the outputs' ancestor cone (output-preserving)
  *   program  (P, program_stride) bytes, written
- *   order    (P, N) int16 row order, -1 padded (StackedNetworks.order), or NULL
+ *   order    (P, N) int16 row order, -1 padded (StackedNetworks.order), or NULL.
+ *            With NULL the programs are built from a level-synchronous Kahn
+ *            (same levels, cycles and programs' results, no per-node order);
+ *            with a buffer the reference's one-node-per-step order is emitted.
+ *            Repeated enabled (src, dst) pairs follow the reference: the last
+ *            connection row wins, and with N <= 64 the genome reads as cyclic
  *   conn_rows (P, C, 2) int16 (src row, dst row) of enabled conns, -1 else, or NULL
  *   io_rows  (P, I+O) int32 rows of keys 0..I+O-1, or NULL
  *   status   (P,) int32 ST_* bits (1 cyclic, 2 bad act, 4 bad agg, 8 bad key,
@@ -68,7 +75,8 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
  *            so a launch per slot-count bucket raises occupancy
  *   variant  0 auto, 1/3 = tile kernel 1 input/thread (128/64 threads),
  *            2/5 = 2 inputs/thread (128/64 threads), 4 = 4 inputs/thread,
- *            8 = warp-per-genome kernel (small B) */
+ *            8 = warp-per-genome kernel (small B), 10 = split programs (the only
+ *            kernel for them); bits 8..15 = tiles per CTA (0 = 4) */
 int an_forward(const void* program, int64_t program_stride, int N, int C, int precision,
                const int32_t* maxdims_host, const int32_t* genome_ids, const void* inputs,
                int64_t input_genome_stride, int64_t P, int B, int I, int O, void* outputs, int variant,
