@@ -627,7 +627,7 @@ __device__ __forceinline__ void input_issue(float (&v)[2 * GW * S], const uint32
                                             uint32_t cmask) {
 #pragma unroll
   for (int q = 0; q < 2 * GW; ++q)
-    if (q % GW < G) tmem_ld_cols<S>(tlane + (col[q] & cmask), v + q * S);
+    if (q % GW < G) tmem_ld_cols<S>(tlane + col[q], v + q * S);  // columns < the allocation by construction
 }
 template <int S, int G, int GW, bool EXACT>
 __device__ __forceinline__ void input_fma(float2 (&acc)[G][(S + 1) / 2], const float (&v)[2 * GW * S],
