@@ -2,22 +2,25 @@
 //
 // Replaces arrayneat inference.forward_arrays (inference.py:185-262).
 //
-// Two kernels:
-//   * fwd_tile: one CTA per (genome, tile of NT*S inputs).  Each thread owns S
-//     consecutive inputs; node values live in shared memory as [slot][tile]
-//     (inputs first, staged from HBM with 16-byte loads), so a thread only ever
-//     reads values it wrote itself -- no barrier inside the node sweep.  Steps
-//     are executed a group at a time (<= 4 independent same-level nodes with
-//     interleaved edge lists): the group's nodes accumulate in lock-step as
-//     independent FMA chains, which is what hides shared-memory and MUFU latency
-//     at the occupancy the value tiles allow.  Edge descriptors are warp-uniform
-//     (uniform-register addressed) 16-byte loads, value reads S-wide vector loads.
-//     For large per-genome batches (config 2: B = 4096).
+// Kernels:
+//   * fwd_tile (default for large batches, config 2: B = 4096): one CTA per
+//     (genome, run of tiles of NT*S inputs).  Each thread owns S consecutive
+//     inputs; node values live in shared memory as [slot][tile] (inputs staged
+//     from HBM with coalesced 16-byte loads, the next tile prefetched into L2 by
+//     the TMA engine), so a thread only ever reads values it wrote itself -- no
+//     barrier inside the node sweep.  Steps run a group at a time (<= 4
+//     independent same-level nodes with interleaved edge lists): the group's
+//     nodes accumulate in lock-step as independent FFMA2 chains (two samples
+//     per instruction); padding entries read a zero slot so every round is
+//     unpredicated; program words are warp-uniform 16-byte loads, prefetched
+//     one group ahead.
 //   * fwd_warp: one warp per (genome, input chunk); lanes split a node's incoming
 //     edges and combine with warp-shuffle reductions (sum/product/max/min/mean).
 //     For small batches (XOR B=4, regression B=64, cart-pole B=1) where a
 //     thread-per-input mapping would idle most lanes.  Optionally fuses the
 //     XOR / regression fitness epilogue (problems.py:54-61).
+//   * fwd_split (split programs, opt-in): input values in tensor memory
+//     (tcgen05.st / tcgen05.ld), hidden values in shared memory.
 //
 // Semantics: input rows hold raw inputs and are never
 // activated; node = act(bias + response * agg(w * v)); empty aggregation = 0;
