@@ -18,6 +18,9 @@
 // tanh -> squared error -> running sum) of tile t-1 while the tensor core
 // works on tile t.  Y is never written to memory.
 
+#include <cuda.h>          // CUtensorMap (types only: no link against libcuda)
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled, resolved via cudaGetDriverEntryPoint
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -31,10 +34,13 @@ constexpr int HN_M = 128;          // rows per tile (MMA M)
 constexpr int HN_THREADS = 512;        // 16 warps: warp w reads TMEM lanes 32*(w%4).. of
 constexpr int HN_SETS = HN_THREADS / 128; // genomes (w/4)*HN_G/HN_SETS .. in the epilogue
 
-// K-major, no-swizzle canonical layout (tc.cuh): 16 K-chunks per 8-row block,
-// consecutive 8-row blocks 2048 B apart
-constexpr uint32_t HN_SBO = 2048;
-__device__ __forceinline__ uint32_t km_offset(int row, int k) { return kmajor_offset(row, k, HN_SBO); }
+// K-major, no-swizzle operands laid out as K-chunk slabs: element (row, k) at
+// (k / 4) * LBO + row * 16 + (k % 4) * 4, i.e. core matrices 8 rows x 16 B with
+// SBO = 128 B between 8-row blocks and LBO = rows * 16 B between K chunks.  A
+// slab (all rows of one 4-float K chunk) is one TMA box {4, rows}.
+constexpr uint32_t HN_SBO = 128;
+constexpr uint32_t HN_LBO_A = HN_M * 16;   // 2 KB
+constexpr uint32_t HN_LBO_B = HN_N * 16;   // 4 KB
 
 constexpr uint32_t HN_IDESC = idesc_tf32(HN_M, HN_N);
 
@@ -45,25 +51,24 @@ __device__ __forceinline__ float tanh_approx(float x) {
 }
 
 struct __align__(1024) HnSmem {
-  float b[HN_N * HN_K];          // 64 KB: 4 genomes' W rows, K-major core matrices
-  float a[2][HN_M * HN_K];       // 2 x 32 KB: X tiles
+  float b[HN_N * HN_K];          // 64 KB: 4 genomes' W rows, 16 K-chunk slabs of 256 rows
+  float a[2][HN_M * HN_K];       // 2 x 32 KB: X tiles, 16 K-chunk slabs of 128 rows
   float part[HN_THREADS / 32][HN_G];
   uint64_t mma_bar[2];
+  uint64_t load_bar[2];          // TMA completion of A[stage] (and of B with stage 0's first use)
   uint32_t tmem_base;
 };
 
-// stage one 128 x 64 fp32 tile of X (rows r0..r0+127) into the core-matrix layout
-__device__ __forceinline__ void load_a_tile(float* a, const float* __restrict__ X, int r0) {
+// one 128 x 64 tile of X (rows r0..) by TMA: 16 slab copies of 2 KB
+__device__ __forceinline__ void tma_a_tile(float* a, const void* tx, int r0, uint32_t bar, bool arrive = true) {
+  if (arrive) mbar_expect_tx(bar, HN_M * HN_K * 4);
   const uint32_t base = smem_u32(a);
-  for (int c = threadIdx.x; c < HN_M * HN_K / 4; c += HN_THREADS) {
-    const int row = c >> 4, k = (c & 15) * 4;
-    cp_async16(base + km_offset(row, k), X + (int64_t)(r0 + row) * HN_K + k);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
+#pragma unroll
+  for (int kc = 0; kc < HN_K / 4; ++kc) tma_load_2d(base + kc * HN_LBO_A, tx, kc * 4, r0, bar);
 }
 
 __global__ void __launch_bounds__(HN_THREADS, 1)
-substrate_kernel(const float* __restrict__ W, int64_t P, const float* __restrict__ X,
+substrate_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, int64_t P,
                  const float* __restrict__ target, int S, double* __restrict__ fitness) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   HnSmem& sm = *reinterpret_cast<HnSmem*>(smem_raw);
@@ -80,24 +85,20 @@ substrate_kernel(const float* __restrict__ W, int64_t P, const float* __restrict
   if (tid == 0) {
     mbar_init(smem_u32(&sm.mma_bar[0]), 1);
     mbar_init(smem_u32(&sm.mma_bar[1]), 1);
+    mbar_init(smem_u32(&sm.load_bar[0]), 1);
+    mbar_init(smem_u32(&sm.load_bar[1]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  // B operand: rows n = g*64 + k (output node k of genome g), K = input node j
-  {
+    // B operand: rows n = g*64 + k (output node k of genome g) = rows g0*64.. of
+    // W viewed as (P*64, 64); rows past P*64 come back as zeros (TMA bounds)
+    // B and the first A tile complete one phase of load_bar[0]: one arrival
+    // carrying both transaction counts
+    const uint32_t bar = smem_u32(&sm.load_bar[0]);
+    mbar_expect_tx(bar, (HN_N + HN_M) * HN_K * 4);
     const uint32_t base = smem_u32(sm.b);
-    for (int c = tid; c < HN_N * HN_K / 4; c += HN_THREADS) {
-      const int row = c >> 4, k = (c & 15) * 4;
-      const int g = row >> 6;
-      if (g < ng) {
-        cp_async16(base + km_offset(row, k), W + ((g0 + g) * HN_N1 + (row & 63)) * (int64_t)HN_K + k);
-      } else {
-        float* dst = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sm.b) + km_offset(row, k));
-        dst[0] = dst[1] = dst[2] = dst[3] = 0.f;
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+#pragma unroll
+    for (int kc = 0; kc < HN_K / 4; ++kc) tma_load_2d(base + kc * HN_LBO_B, &tmap_w, kc * 4, (int)(g0 * HN_N1), bar);
+    tma_a_tile(sm.a[0], &tmap_x, 0, bar, false);
   }
-  load_a_tile(sm.a[0], X, 0);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -132,31 +133,32 @@ substrate_kernel(const float* __restrict__ W, int64_t P, const float* __restrict
     }
   };
 
+  uint32_t lphase[2] = {0u, 0u};
   for (int t = 0; t < tiles; ++t) {
     const int stage = t & 1;
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async data -> tensor core
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();  // A[t] (and B) staged; epilogue(t-2) done with accumulator `stage`
+    __syncthreads();  // epilogue(t-2) is done with accumulator `stage`
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tid == 0) {
+      mbar_wait(smem_u32(&sm.load_bar[stage]), lphase[stage]);  // A[t] (and B) landed
       const uint32_t a0 = smem_u32(sm.a[stage]), b0 = smem_u32(sm.b);
 #pragma unroll
-      for (int kk = 0; kk < HN_K / 8; ++kk)  // K = 8 tf32 per instruction = 2 core matrices
-        mma_tf32(tmem + (uint32_t)(stage * HN_N), smem_desc(a0 + kk * 256, HN_SBO), smem_desc(b0 + kk * 256, HN_SBO), HN_IDESC,
-                 kk > 0 ? 1u : 0u);
+      for (int kk = 0; kk < HN_K / 8; ++kk)  // K = 8 tf32 per instruction = 2 K-chunk slabs
+        mma_tf32(tmem + (uint32_t)(stage * HN_N), smem_desc(a0 + kk * 2 * HN_LBO_A, HN_SBO, HN_LBO_A),
+                 smem_desc(b0 + kk * 2 * HN_LBO_B, HN_SBO, HN_LBO_B), HN_IDESC, kk > 0 ? 1u : 0u);
       mma_commit(smem_u32(&sm.mma_bar[stage]));
     }
+    lphase[stage] ^= 1u;
     if (t >= 1) {
       // MMA t-1 finished -> its A buffer (the other one) is free and its accumulator ready
       mbar_wait(smem_u32(&sm.mma_bar[stage ^ 1]), phase[stage ^ 1]);
       phase[stage ^ 1] ^= 1u;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (t + 1 < tiles) load_a_tile(sm.a[stage ^ 1], X, (t + 1) * HN_M);
+      if (tid == 0 && t + 1 < tiles) tma_a_tile(sm.a[stage ^ 1], &tmap_x, (t + 1) * HN_M, smem_u32(&sm.load_bar[stage ^ 1]));
       epilogue(t - 1, stage ^ 1);
-    } else if (t + 1 < tiles) {
+    } else if (tid == 0 && t + 1 < tiles) {
       // the other A buffer has never been used
-      load_a_tile(sm.a[stage ^ 1], X, (t + 1) * HN_M);
+      tma_a_tile(sm.a[stage ^ 1], &tmap_x, (t + 1) * HN_M, smem_u32(&sm.load_bar[stage ^ 1]));
     }
   }
   {
@@ -206,10 +208,38 @@ int an_substrate_fitness(const float* W, int64_t P, const float* X, const float*
   if (P < 0 || S <= 0 || S % HN_M != 0) return -1;
   if (P == 0) return 0;
   if (!W || !X || !target || !fitness) return -2;
+  if (((uintptr_t)W | (uintptr_t)X) & 15) return -2;
+  // TMA descriptors: W as a (P*64, 64) and X as an (S, 64) row-major fp32 matrix,
+  // boxes of one 4-float K chunk x all tile rows
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess || !encode)
+      return -9;
+  }
+  CUtensorMap tw, tx;
+  const cuuint32_t estr[2] = {1, 1};
+  {
+    const cuuint64_t dims[2] = {HN_K, (cuuint64_t)P * HN_N1}, strides[1] = {HN_K * 4};
+    const cuuint32_t box[2] = {4, HN_N};
+    if (encode(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(W), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -9;
+  }
+  {
+    const cuuint64_t dims[2] = {HN_K, (cuuint64_t)S}, strides[1] = {HN_K * 4};
+    const cuuint32_t box[2] = {4, HN_M};
+    if (encode(&tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -9;
+  }
   const int smem = (int)sizeof(HnSmem) + 1024;
   cudaFuncSetAttribute(substrate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int64_t blocks = (P + HN_G - 1) / HN_G;
-  substrate_kernel<<<(unsigned)blocks, HN_THREADS, smem, (cudaStream_t)stream>>>(W, P, X, target, S, fitness);
+  substrate_kernel<<<(unsigned)blocks, HN_THREADS, smem, (cudaStream_t)stream>>>(tw, tx, P, target, S, fitness);
   TNEAT_CHECK_LAUNCH();
   return 0;
 }

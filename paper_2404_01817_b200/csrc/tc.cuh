@@ -19,13 +19,24 @@ __device__ __forceinline__ uint32_t kmajor_offset(int row, int k, uint32_t sbo) 
   return (uint32_t)(row >> 3) * sbo + (uint32_t)((k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
 }
 
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t sbo) {
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t sbo, uint32_t lbo = 128) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
-  d |= (uint64_t)(128 >> 4) << 16;               // leading byte offset (K direction)
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;    // leading byte offset (K direction)
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;    // stride byte offset (M/N direction)
   d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
   return d;                                      // base offset 0, layout SWIZZLE_NONE
+}
+
+// TMA: 2-D tensor tile global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 
 // instruction descriptor: kind::tf32, D = F32, A = B = TF32, both K-major
