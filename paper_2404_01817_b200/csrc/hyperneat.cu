@@ -10,9 +10,9 @@
 //
 // This is the only dense contraction of the system, so it is the one kernel on
 // tcgen05: each CTA owns 4 genomes (N = 4 x 64 = 256 accumulator columns),
-// their W rows are the B operand (K-major, staged once); the CTA streams
+// their W rows are the B operand (K-major, loaded once by TMA); the CTA streams
 // 128-row tiles of X as the A operand through two shared-memory buffers
-// (cp.async), one elected thread issues `tcgen05.mma.kind::tf32` (M=128,
+// (TMA 2-D tensor copies completing on mbarriers), one elected thread issues `tcgen05.mma.kind::tf32` (M=128,
 // N=256, K=8 per instruction, 8 per tile) into one of two TMEM accumulators
 // (2 x 256 columns), and the four warps run the fused epilogue (tcgen05.ld ->
 // tanh -> squared error -> running sum) of tile t-1 while the tensor core
