@@ -155,6 +155,37 @@ __device__ void warp_exclusive_scan(const int32_t* cnt, int32_t* out, int n) {
   __syncwarp();
 }
 
+// Stable scatter of n edge keys into buckets by the 16-bit field at `shift`
+// (bucket b starts at start[b]; cursor[] zeroed by the caller).  Chunks of 32
+// keep the input order: lanes with equal buckets rank themselves with
+// __match_any_sync and the lowest of them advances the bucket cursor.  With
+// `succ`, also writes the destination row (bits 48..63) of each key at its
+// position (the CSR by source).
+__device__ void stable_scatter(const uint64_t* in, uint64_t* out, int n, int shift, const int32_t* start,
+                               int32_t* cursor, uint16_t* succ) {
+  const int lane = threadIdx.x & 31;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const bool valid = i < n;
+    const uint64_t k = valid ? in[i] : 0ull;
+    const uint32_t b = valid ? (uint32_t)((k >> shift) & 0xFFFF) : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    const int leader = __ffs(peers) - 1;
+    int old = 0;
+    if (valid && lane == leader) {
+      old = cursor[b];
+      cursor[b] = old + __popc(peers);
+    }
+    old = __shfl_sync(0xffffffffu, old, leader);
+    if (valid) {
+      const int pos = start[b] + old + __popc(peers & ((1u << lane) - 1));
+      out[pos] = k;
+      if (succ) succ[pos] = (uint16_t)((k >> 48) & 0xFFFF);
+    }
+    __syncwarp();
+  }
+}
+
 // row of `key` among the sorted live (key<<16|row) pairs, or -1
 __device__ inline int lookup_row(const uint64_t* skey, int Npad, uint64_t key) {
   int lo = 0, hi = Npad;
@@ -280,22 +311,16 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   warp_exclusive_scan(s.outdeg, s.su_start, N);
   for (int r = lane; r < N; r += 32) { s.outdeg[r] = 0; s.lvl[r] = 0; }  // cursors
   __syncwarp();
-  for (int e = lane; e < n_en; e += 32) {
-    const uint64_t k = s.ekey2[e];
-    const int dr = (int)((k >> 48) & 0xFFFF), sr = (int)((k >> 32) & 0xFFFF);
-    s.ekey[s.in_start[dr] + atomicAdd(&s.lvl[dr], 1)] = k;
-    s.succ[s.su_start[sr] + atomicAdd(&s.outdeg[sr], 1)] = (uint16_t)dr;
-  }
+  // two stable, order-preserving scatters (LSD radix by source, then by
+  // destination): the edges start in connection-row order, so every
+  // destination bucket ends up sorted by (source row, connection row)
+  stable_scatter(s.ekey2, s.ekey, n_en, 32, s.su_start, s.outdeg, s.succ);
+  stable_scatter(s.ekey, s.ekey2, n_en, 48, s.in_start, s.lvl, nullptr);
+  for (int e = lane; e < n_en; e += 32) s.ekey[e] = s.ekey2[e];
   __syncwarp();
   int shadowed_any = 0;
-  for (int r = lane; r < N; r += 32) {  // insertion sort of each (small) bucket
+  for (int r = lane; r < N; r += 32) {
     const int b0 = s.in_start[r], b1 = s.in_start[r + 1];
-    for (int i = b0 + 1; i < b1; ++i) {
-      const uint64_t x = s.ekey[i];
-      int j = i - 1;
-      while (j >= b0 && s.ekey[j] > x) { s.ekey[j + 1] = s.ekey[j]; --j; }
-      s.ekey[j + 1] = x;
-    }
     // repeated enabled (src, dst) pairs: the reference's dense incoming keeps
     // the last connection row (inference.py:108-112); the earlier ones are
     // shadowed -- counted here, removed below
