@@ -19,3 +19,18 @@ print("groups/genome", ng.mean(), "steps", steps.mean(), "edge entries", edges.m
 print("group size hist", np.bincount(sizes))
 print("rounds mean", rounds.mean(), "hist", np.bincount(np.minimum(rounds, 40))[:41])
 print("edge-slots per genome (sum gw*rounds)", (np.where(sizes==3,4,sizes)*rounds).sum()/1000)
+cnts = []
+for p in range(1000):
+    g = prog[p, 48:48 + 16 * ng[p]].reshape(-1, 16)
+    cnts.append(g[:, 8:16].copy().view(np.uint16).astype(np.int64).sum())
+print("real entries / genome", np.mean(cnts), "padding frac", 1 - np.sum(cnts) / (np.where(sizes==3,4,sizes)*rounds).sum())
+lv = []
+sp, _ = tn.transform_arrays(n, c, 32, 8, layout="split")
+pr = sp.program.cpu().numpy()
+hd = pr[:, :32].view(np.int32)
+cin = []; ch = []
+for p in range(1000):
+    g = pr[p, 48:48 + 32 * hd[p, 7]].reshape(-1, 32)
+    cin.append(g[:, 16:24].copy().view(np.uint16).astype(np.int64).sum())
+    ch.append(g[:, 24:32].copy().view(np.uint16).astype(np.int64).sum())
+print("input-sourced edges / genome", np.mean(cin), "hidden-sourced", np.mean(ch))

@@ -15,7 +15,12 @@ ap.add_argument("--pop", type=int, default=10000)
 ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--reps", type=int, default=4)
 ap.add_argument("--layout", default="auto")
+ap.add_argument("--lib", default=None, help="alternative libtneat.so build (tuning experiments)")
+ap.add_argument("--fwd-reps", type=int, default=10)
 a = ap.parse_args()
+if a.lib:
+    from paper_2404_01817_b200 import _native
+    _native.LIB_PATH = os.path.abspath(a.lib)
 n, c = synthetic_population(a.pop, 128, 512, 32, 8, seed=20261018)
 nodes, conns = torch.from_numpy(n).cuda(), torch.from_numpy(c).cuda()
 x = torch.randn((a.pop, 4096, 32), device="cuda")
@@ -37,3 +42,13 @@ for rep in range(a.reps):
     t4 = time.perf_counter()
     print(f"transform {1e3*(t1-t0):.2f} ms finalize {1e3*(t2-t1):.2f} plan {1e3*(t3-t2):.2f} "
           f"forward {1e3*(t4-t3):.2f} buckets {len(plan)} maxdims {st.maxdims}", flush=True)
+evs = []
+for _ in range(a.fwd_reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    tn.forward_device(st, x, out, variant=a.variant)
+    e1.record()
+    torch.cuda.synchronize()
+    evs.append(e0.elapsed_time(e1))
+evs.sort()
+print(f"{a.lib or 'libtneat.so'} forward median {evs[len(evs) // 2]:.3f} ms min {evs[0]:.3f} ms", flush=True)
