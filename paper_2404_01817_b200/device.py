@@ -24,6 +24,33 @@ def stream_handle(stream: torch.cuda.Stream | None = None) -> int:
     return int(s.cuda_stream)
 
 
+_STAGE_BYTES = 32 << 20
+_stage = {"bufs": None, "events": [None, None]}
+
+
+def _upload_staged(t: torch.Tensor, dev: torch.device) -> torch.Tensor:
+    """Large pageable host tensor -> device through two pinned 32 MB staging
+    buffers: the DMA of chunk k overlaps the host copy of chunk k+1."""
+    if _stage["bufs"] is None:
+        _stage["bufs"] = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    src = t.reshape(-1).view(torch.uint8)
+    out = torch.empty(t.shape, dtype=t.dtype, device=dev)
+    dst = out.reshape(-1).view(torch.uint8)
+    n = src.numel()
+    for k, lo in enumerate(range(0, n, _STAGE_BYTES)):
+        hi = min(n, lo + _STAGE_BYTES)
+        slot = k & 1
+        if _stage["events"][slot] is not None:
+            _stage["events"][slot].synchronize()
+        buf = _stage["bufs"][slot][: hi - lo]
+        buf.copy_(src[lo:hi])
+        dst[lo:hi].copy_(buf, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        _stage["events"][slot] = ev
+    return out
+
+
 def to_device(x, dtype: torch.dtype) -> torch.Tensor:
     """numpy / torch (any device) -> contiguous device tensor of ``dtype``."""
     dev = device()
@@ -32,10 +59,54 @@ def to_device(x, dtype: torch.dtype) -> torch.Tensor:
     else:
         t = torch.from_numpy(np.ascontiguousarray(x))
     if t.device != dev:
-        t = t.to(dev, non_blocking=t.is_pinned())
+        if t.device.type == "cpu" and not t.is_pinned() and t.numel() * t.element_size() > 2 * _STAGE_BYTES:
+            t = _upload_staged(t.contiguous(), dev)
+        else:
+            t = t.to(dev, non_blocking=t.is_pinned())
     if t.dtype != dtype:
         t = t.to(dtype)
     return t.contiguous()
+
+
+class _PinnedRing:
+    """A few reusable pinned staging buffers for small host->device uploads:
+    the copy is asynchronous on the current stream and a buffer is reused
+    only after its previous copy has completed (event), so planning inside a
+    copy/compute pipeline never synchronizes a stream."""
+
+    def __init__(self, n: int = 4):
+        self.bufs = [None] * n
+        self.events = [None] * n
+        self.k = 0
+
+    def upload(self, arr: np.ndarray, dev: torch.device) -> torch.Tensor:
+        src = torch.from_numpy(np.ascontiguousarray(arr))
+        nbytes = src.numel() * src.element_size()
+        slot = self.k
+        self.k = (self.k + 1) % len(self.bufs)
+        if self.events[slot] is not None:
+            self.events[slot].synchronize()
+        buf = self.bufs[slot]
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, pin_memory=True)
+            self.bufs[slot] = buf
+        staged = buf[:nbytes].view(src.dtype).view(src.shape)
+        staged.copy_(src)
+        out = torch.empty(src.shape, dtype=src.dtype, device=dev)
+        out.copy_(staged, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.events[slot] = ev
+        return out, ev
+
+
+_RING = _PinnedRing()
+
+
+def upload_async(arr: np.ndarray, dev: torch.device) -> tuple[torch.Tensor, torch.cuda.Event]:
+    """Small numpy array -> device tensor without a stream synchronization;
+    consumers on other streams wait on the returned event."""
+    return _RING.upload(arr, dev)
 
 
 def ptr(t: torch.Tensor | None) -> int | None:

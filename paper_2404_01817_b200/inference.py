@@ -34,7 +34,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .device import device, ptr, stream_handle, to_device
+from .device import upload_async, device, ptr, stream_handle, to_device
 from .errors import ConfigError, CycleDetected, IntegrityError, InvalidInput
 from .functions import DEFAULT_REGISTRY, check_registry
 
@@ -149,12 +149,19 @@ class StackedNetworks:
         return TransformedNetwork(sub)
 
     def select(self, idx) -> "StackedNetworks":
-        """Row subset (a view on the same device buffers where possible)."""
-        return StackedNetworks(self.nodes_dev[idx], self.conns_dev[idx], self.num_inputs,
-                               self.num_outputs, self.program[idx],
-                               None if self.order_dev is None else self.order_dev[idx],
-                               self.conn_rows[idx], self.io_rows[idx], self.status_dev[idx],
-                               self.maxdims, self.precision, self.mode)
+        """Row subset (a view on the same device buffers where possible).  The
+        host copies of status and slot counts carry over, so planning a subset's
+        launches needs no device read-back."""
+        sub = StackedNetworks(self.nodes_dev[idx], self.conns_dev[idx], self.num_inputs,
+                              self.num_outputs, self.program[idx],
+                              None if self.order_dev is None else self.order_dev[idx],
+                              self.conn_rows[idx], self.io_rows[idx], self.status_dev[idx],
+                              self.maxdims, self.precision, self.mode)
+        if isinstance(idx, slice):
+            for k in ("status", "slots"):
+                if k in self._cache:
+                    sub._cache[k] = self._cache[k][idx]
+        return sub
 
     @classmethod
     def from_networks(cls, networks: list) -> "StackedNetworks":
@@ -342,7 +349,9 @@ def _bucket_plan(stacked: StackedNetworks, variant: int) -> list:
     # slot counts are small integers: a 16-bit key makes numpy's stable sort a radix sort
     order = np.argsort(np.minimum(slots, 65535).astype(np.uint16), kind="stable").astype(np.int32)
     sorted_slots = slots[order]
-    ids = torch.from_numpy(order).to(stacked.program.device)  # 4P bytes; no pinned allocation per plan
+    # no stream sync (plans are made inside copy/compute pipelines); launches wait on the upload's event
+    ids, ev = upload_async(order, stacked.program.device)
+    stacked._cache[("plan_ready", variant)] = ev
     _, ms, me = stacked.maxdims
     prog = 32 * ms + (16 * me if stacked.precision & FMT_F64 else 8 * me + 16) + 16
     if variant == V_SPLIT:  # fwd_split_kernel: 4 warps, 256 inputs per tile, hidden slots only
@@ -398,7 +407,9 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
             stream_handle(stream))
     v &= 0xF
     if (v in _TILE_TT or v == V_SPLIT) and bucketed and pop > 1:
-        for ids, md in _bucket_plan(stacked, v):
+        plan = _bucket_plan(stacked, v)
+        (stream or torch.cuda.current_stream()).wait_event(stacked._cache[("plan_ready", v)])
+        for ids, md in plan:
             _native.call("an_forward", *args, _maxdims_arg(stacked, md), ptr(ids), ptr(inputs), gstride,
                          int(ids.numel()), *tail)
     else:
@@ -417,24 +428,38 @@ def _maxdims_arg(stacked: StackedNetworks, dims=None) -> int:
     return ctypes.addressof(arr)
 
 
+def _chunk_bounds(pop: int, per: int, first: int) -> list:
+    """Genome ranges of the copy/compute pipeline: the first chunks ramp up
+    from ``first`` genomes (short pipeline fill), then ``per`` each."""
+    bounds, lo, size = [], 0, max(1, min(first, per))
+    while lo < pop:
+        hi = min(pop, lo + size)
+        bounds.append((lo, hi))
+        lo, size = hi, min(per, 2 * size)
+    return bounds
+
+
 def _host_forward_pipelined(stacked: StackedNetworks, x: torch.Tensor, out_host: torch.Tensor,
                             chunk_bytes: int = 256 << 20, variant: int = 0) -> torch.Tensor:
     """Host (P,B,I) -> host (P,B,O) in genome chunks: H2D copy of chunk k+1
     and D2H of chunk k-1 overlap the kernel on chunk k (two copy streams,
-    double-buffered device staging).  Pinned host tensors make the copies
-    asynchronous DMA."""
+    double-buffered device staging; chunks ramp up from 1/8 of the chunk size
+    so the pipeline fills quickly).  Pinned host tensors make the copies
+    asynchronous DMA; the per-chunk launch plans come from the host copy of
+    the slot counts (no device read-back inside the loop)."""
     pop, b, i = x.shape
     o = stacked.num_outputs
     dt = _TORCH_DT[stacked.precision]
     dev = device()
     per = max(1, int(chunk_bytes // max(1, b * i * x.element_size())))
+    if "slots" not in stacked._cache:
+        stacked._cache["slots"] = stacked.program[:, 8:12].contiguous().view(torch.int32).reshape(-1).cpu().numpy()
     bufs_in = [torch.empty((min(per, pop), b, i), dtype=dt, device=dev) for _ in range(2)]
     bufs_out = [torch.empty((min(per, pop), b, o), dtype=dt, device=dev) for _ in range(2)]
     h2d, comp, d2h = torch.cuda.Stream(), torch.cuda.current_stream(), torch.cuda.Stream()
     in_free = [None, None]
     out_free = [None, None]
-    for k, lo in enumerate(range(0, pop, per)):
-        hi = min(pop, lo + per)
+    for k, (lo, hi) in enumerate(_chunk_bounds(pop, per, max(1, per // 8))):
         slot = k & 1
         with torch.cuda.stream(h2d):
             if in_free[slot] is not None:
