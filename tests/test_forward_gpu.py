@@ -247,3 +247,26 @@ def test_duplicate_pairs_match_reference(tn, name):
         st2, _ = tn.transform_arrays(g["nodes"][ok], g["conns"][ok], 2, 1, precision="f64")
         out = tn.forward_arrays(st2, None, g["inputs"][ok])
         np.testing.assert_allclose(out, g["outputs"][ok], rtol=1e-9, atol=1e-9)
+
+
+def test_large_host_uploads_staged(tn):
+    """Pageable host arrays above the staging threshold go through the pinned
+    double buffer (device.to_device): bitwise the same tensor, and the same
+    programs as a transform of device-resident genomes.  Subsets keep the
+    host slot counts (launch plans without read-back)."""
+    import torch
+    from oracle.arrayneat_oracle import synthetic_population
+    from paper_2404_01817_b200.device import _STAGE_BYTES, to_device
+    big = np.random.default_rng(9).standard_normal((3 * _STAGE_BYTES) // 8 + 123)
+    assert torch.equal(to_device(big, torch.float64).cpu(), torch.from_numpy(big))
+    nodes, conns = synthetic_population(40, 128, 512, 32, 8, seed=82)
+    reps = (2 * _STAGE_BYTES) // conns[:1].nbytes // 40 + 1
+    nodes, conns = np.tile(nodes, (reps, 1, 1)), np.tile(conns, (reps, 1, 1))
+    assert conns.nbytes > 2 * _STAGE_BYTES
+    a, _ = tn.transform_arrays(nodes, conns, 32, 8)
+    b, _ = tn.transform_arrays(torch.from_numpy(nodes).cuda(), torch.from_numpy(conns).cuda(), 32, 8)
+    assert torch.equal(a.program, b.program)
+    sub = a.select(slice(5, 17))
+    np.testing.assert_array_equal(sub._cache["slots"], a._cache["slots"][5:17])
+    x = torch.randn(12, 300, 32, device="cuda")
+    assert torch.equal(tn.forward_device(sub, x), tn.forward_device(b.select(slice(5, 17)), x))
