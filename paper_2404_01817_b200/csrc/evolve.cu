@@ -592,6 +592,186 @@ __global__ void distance_kernel(const double* __restrict__ n1, const double* __r
   }
 }
 
+// Distance of every genome against a small set of representatives (speciate:
+// pair_mode 0, R reps x P genomes; founding rounds: pair_mode 1, Q == 1).
+// Persistent CTAs stage the Q representatives and their key -> row maps in
+// shared memory once, then one thread per (genome, representative) pair walks
+// genome 1's rows in order: the homologous terms are summed as they are found,
+// which is the reference's row order (np.bincount), so the result is bitwise
+// the warp kernel's.  Homolog lookup: same row first, else a binary search in
+// the representative's sorted (key bits, row) map -- the smallest matching row,
+// as the reference's first-match scan.  Keys compare as doubles: -0 is mapped
+// to +0 and NaN rows never match.
+__device__ __forceinline__ uint64_t key_bits(double k) { return (uint64_t)__double_as_longlong(k == 0.0 ? 0.0 : k); }
+
+struct RepSmem {
+  double* nodes;    // [Q][N*5]
+  double* conns;    // [Q][C*4]
+  uint64_t* nkey;   // [Q][N] sorted node key bits (NaN rows: U64 max, last)
+  uint16_t* nrow;   // [Q][N]
+  uint64_t* ckin;   // [Q][C] sorted (in, out) key bits
+  uint64_t* ckout;
+  uint16_t* crow;
+  int* live;        // [Q][2] live nodes, live conns
+};
+
+__host__ __device__ inline int64_t rep_smem_bytes(int Q, int N, int C, RepSmem* s, uint8_t* base) {
+  int64_t o = 0;
+  auto take = [&](int64_t bytes, int64_t al) { o = (o + al - 1) / al * al; const int64_t at = o; o += bytes; return at; };
+  const int64_t a_n = take(8ll * Q * N * 5, 16), a_c = take(8ll * Q * C * 4, 16);
+  const int64_t a_nk = take(8ll * Q * N, 8), a_ck = take(8ll * Q * C, 8), a_co = take(8ll * Q * C, 8);
+  const int64_t a_nr = take(2ll * Q * N, 2), a_cr = take(2ll * Q * C, 2), a_l = take(8ll * Q, 4);
+  if (s) {
+    s->nodes = (double*)(base + a_n); s->conns = (double*)(base + a_c);
+    s->nkey = (uint64_t*)(base + a_nk); s->ckin = (uint64_t*)(base + a_ck); s->ckout = (uint64_t*)(base + a_co);
+    s->nrow = (uint16_t*)(base + a_nr); s->crow = (uint16_t*)(base + a_cr); s->live = (int*)(base + a_l);
+  }
+  return (o + 15) / 16 * 16;
+}
+
+__global__ void distance_reps_kernel(const double* __restrict__ n1, const double* __restrict__ c1, int64_t P,
+                                     const double* __restrict__ n2, const double* __restrict__ c2, int Q, int N,
+                                     int C, double cd, double ch, double* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  RepSmem s;
+  rep_smem_bytes(Q, N, C, &s, smem);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // stage the representatives (coalesced) and build their maps by ranking:
+  // entry i goes to position #{j : (key_j, j) < (key_i, i)} (keys unique up to
+  // NaN / duplicates; ties broken by row, smallest first)
+  for (int64_t i = tid; i < (int64_t)Q * N * 5; i += nt) s.nodes[i] = n2[i];
+  for (int64_t i = tid; i < (int64_t)Q * C * 4; i += nt) s.conns[i] = c2[i];
+  __syncthreads();
+  for (int i = tid; i < Q * N; i += nt) {
+    const int q = i / N, r = i - q * N;
+    const double* rows = s.nodes + (int64_t)q * N * 5;
+    const double k = rows[r * 5];
+    const uint64_t kb = is_nan(k) ? ~0ull : key_bits(k);
+    int rank = 0;
+    for (int j = 0; j < N; ++j) {
+      const double kj = rows[j * 5];
+      const uint64_t b = is_nan(kj) ? ~0ull : key_bits(kj);
+      rank += (b < kb || (b == kb && j < r)) ? 1 : 0;
+    }
+    s.nkey[q * N + rank] = kb;
+    s.nrow[q * N + rank] = (uint16_t)r;
+  }
+  for (int i = tid; i < Q * C; i += nt) {
+    const int q = i / C, r = i - q * C;
+    const double* rows = s.conns + (int64_t)q * C * 4;
+    const double a = rows[r * 4], b = rows[r * 4 + 1];
+    const bool dead = is_nan(a) || is_nan(b);
+    const uint64_t ka = dead ? ~0ull : key_bits(a), kb = dead ? ~0ull : key_bits(b);
+    int rank = 0;
+    for (int j = 0; j < C; ++j) {
+      const double aj = rows[j * 4], bj = rows[j * 4 + 1];
+      const bool dj = is_nan(aj) || is_nan(bj);
+      const uint64_t xa = dj ? ~0ull : key_bits(aj), xb = dj ? ~0ull : key_bits(bj);
+      rank += (xa < ka || (xa == ka && (xb < kb || (xb == kb && j < r)))) ? 1 : 0;
+    }
+    s.ckin[q * C + rank] = ka;
+    s.ckout[q * C + rank] = kb;
+    s.crow[q * C + rank] = (uint16_t)r;
+  }
+  for (int q = tid; q < Q; q += nt) {
+    int ln = 0, lc = 0;
+    for (int r = 0; r < N; ++r) ln += is_nan(s.nodes[(int64_t)q * N * 5 + r * 5]) ? 0 : 1;
+    for (int r = 0; r < C; ++r) lc += is_nan(s.conns[(int64_t)q * C * 4 + r * 4]) ? 0 : 1;
+    s.live[2 * q] = ln;
+    s.live[2 * q + 1] = lc;
+  }
+  __syncthreads();
+
+  const int gpb = nt / Q;  // genomes per CTA pass
+  if (tid >= gpb * Q) return;
+  const int q = tid % Q, gl = tid / Q;
+  const double* b = s.nodes + (int64_t)q * N * 5;
+  const double* bc = s.conns + (int64_t)q * C * 4;
+  const uint64_t* nk = s.nkey + (int64_t)q * N;
+  const uint16_t* nr = s.nrow + (int64_t)q * N;
+  const uint64_t* ki = s.ckin + (int64_t)q * C;
+  const uint64_t* ko = s.ckout + (int64_t)q * C;
+  const uint16_t* cr = s.crow + (int64_t)q * C;
+  for (int64_t p = (int64_t)blockIdx.x * gpb + gl; p < P; p += (int64_t)gridDim.x * gpb) {
+    const double* a = n1 + p * N * 5;
+    const double* ac = c1 + p * C * 4;
+    int live1 = 0, hom_n = 0, clive1 = 0, hom_c = 0;
+    double ns = 0.0, cs = 0.0;
+    // rows in batches of 4, every load of a batch issued before its rows are
+    // processed (memory-level parallelism for the per-thread row walk)
+    for (int r0 = 0; r0 < N; r0 += 4) {
+      double x[20];
+#pragma unroll
+      for (int u = 0; u < 20; ++u) x[u] = r0 * 5 + u < N * 5 ? __ldg(a + r0 * 5 + u) : nanv();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u;
+        const double k = x[u * 5];
+        if (r >= N || is_nan(k)) continue;
+        ++live1;
+        int o = -1;
+        if (b[r * 5] == k) {
+          o = r;
+        } else {
+          const uint64_t kb = key_bits(k);
+          int lo = 0, hi = N;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (nk[mid] < kb) lo = mid + 1; else hi = mid;
+          }
+          if (lo < N && nk[lo] == kb) o = nr[lo];
+        }
+        if (o >= 0) {
+          ++hom_n;
+          const double* y = b + o * 5;
+          double v = __dadd_rn(fabs(__dsub_rn(x[u * 5 + 1], y[1])), fabs(__dsub_rn(x[u * 5 + 2], y[2])));
+          v = __dadd_rn(v, x[u * 5 + 3] != y[3] ? 1.0 : 0.0);
+          v = __dadd_rn(v, x[u * 5 + 4] != y[4] ? 1.0 : 0.0);
+          const double t = __ddiv_rn(v, 4.0);
+          if (!is_nan(t)) ns = __dadd_rn(ns, t);
+        }
+      }
+    }
+    for (int r0 = 0; r0 < C; r0 += 4) {
+      double x[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) x[u] = r0 * 4 + u < C * 4 ? __ldg(ac + r0 * 4 + u) : nanv();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u;
+        const double i = x[u * 4], j = x[u * 4 + 1];
+        if (r >= C || is_nan(i)) continue;
+        ++clive1;
+        int o = -1;
+        if (bc[r * 4] == i && bc[r * 4 + 1] == j) {
+          o = r;
+        } else if (!is_nan(j)) {
+          const uint64_t ka = key_bits(i), kb = key_bits(j);
+          int lo = 0, hi = C;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (ki[mid] < ka || (ki[mid] == ka && ko[mid] < kb)) lo = mid + 1; else hi = mid;
+          }
+          if (lo < C && ki[lo] == ka && ko[lo] == kb) o = cr[lo];
+        }
+        if (o >= 0) {
+          ++hom_c;
+          const double* y = bc + o * 4;
+          const double t = __ddiv_rn(__dadd_rn(fabs(__dsub_rn(x[u * 4 + 3], y[3])), fabs(__dsub_rn(x[u * 4 + 2], y[2]))), 2.0);
+          if (!is_nan(t)) cs = __dadd_rn(cs, t);
+        }
+      }
+    }
+    const int live2 = s.live[2 * q], clive2 = s.live[2 * q + 1];
+    const int node_dis = (live1 - hom_n) + (live2 - hom_n);
+    const int conn_dis = (clive1 - hom_c) + (clive2 - hom_c);
+    const int dis = node_dis + conn_dis, hom = hom_n + hom_c;
+    const double attr = hom > 0 ? __ddiv_rn(__dadd_rn(ns, cs), (double)hom) : 0.0;
+    const int total = max(live1 + clive1, live2 + clive2);
+    out[(int64_t)q * P + p] = __dadd_rn(__ddiv_rn(__dmul_rn(cd, (double)dis), (double)total), __dmul_rn(ch, attr));
+  }
+}
+
 __global__ void rng_draw_kernel(const uint64_t* __restrict__ keys, int64_t S, uint64_t base, int64_t width,
                                 int normals, double* __restrict__ out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -646,6 +826,33 @@ int an_distance(const double* n1, const double* c1, int64_t P, const double* n2,
   if (P < 0 || Q < 1 || N < 1 || C < 0) return -1;
   if (pair_mode && Q != 1 && Q != P) return -1;
   if (P == 0) return 0;
+  // P genomes against a few representatives: representatives staged once per
+  // persistent CTA (when they fit in shared memory)
+  // (in launches of as many representatives as fit in 110 KB)
+  if ((!pair_mode || Q == 1) && N < 65536 && C < 65536) {
+    int64_t qc = Q < 256 ? Q : 256;
+    while (qc > 1 && rep_smem_bytes((int)qc, N, C, nullptr, nullptr) > 110 * 1024) --qc;
+    if (rep_smem_bytes((int)qc, N, C, nullptr, nullptr) <= 110 * 1024) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int nt = 256;
+      for (int64_t q0 = 0; q0 < Q; q0 += qc) {
+        const int qn = (int)(Q - q0 < qc ? Q - q0 : qc);
+        const int64_t rs = rep_smem_bytes(qn, N, C, nullptr, nullptr);
+        const int gpb = nt / qn;
+        const int64_t tiles = (P + gpb - 1) / gpb;
+        int64_t per_sm = (228ll * 1024) / (rs + 1024);
+        per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+        const int64_t grid = tiles < (int64_t)sms * per_sm ? tiles : (int64_t)sms * per_sm;
+        cudaFuncSetAttribute(distance_reps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs);
+        distance_reps_kernel<<<(unsigned)grid, nt, rs, (cudaStream_t)stream>>>(
+            n1, c1, P, n2 + q0 * N * 5, c2 + q0 * C * 4, qn, N, C, c_disjoint, c_homologous, out + q0 * P);
+        TNEAT_CHECK_LAUNCH();
+      }
+      return 0;
+    }
+  }
   const int64_t per = 8ll * (N + C);
   int wpb = 4;
   while (wpb > 1 && per * wpb > 96 * 1024) wpb >>= 1;

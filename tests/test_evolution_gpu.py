@@ -119,6 +119,40 @@ def test_distance_bit_exact(tn):
                           c["dist_pair"])
 
 
+def test_distance_representatives_kernel_equals_pairwise(tn):
+    """The representative-staged kernel (P genomes x R reps, and P x 1) is
+    bitwise the pair kernel, also for rows that are not aligned with the
+    representative's, -0 keys, repeated keys in a representative (first row
+    wins) and infinite attributes."""
+    import torch
+    c = load_golden("corpus.npz")
+    cfg = _cfg(tn)
+    n, cc = c["nodes"].copy(), c["conns"].copy()
+    rng = np.random.default_rng(5)
+    for i in range(0, n.shape[0], 3):  # misaligned rows
+        n[i] = n[i][rng.permutation(n.shape[1])]
+        cc[i] = cc[i][rng.permutation(cc.shape[1])]
+    live = np.nonzero(~np.isnan(n[4, :, 0]))[0]
+    n[4, live[0], 0] = -0.0 if n[4, live[0], 0] == 0.0 else n[4, live[0], 0]
+    n[5, live[-1], 0] = n[5, live[-2], 0] if len(live) > 1 else n[5, live[-1], 0]  # repeated key (rep 5)
+    lc = np.nonzero(~np.isnan(cc[6, :, 0]))[0]
+    cc[6, lc[0], 3] = np.inf
+    ev = tn.evolution
+    nd, cd = ev._dev64(n), ev._dev64(cc)
+    reps = [0, 4, 5, 6, 9, 17, 33]
+    rn, rc = nd[reps].contiguous(), cd[reps].contiguous()
+    mat = ev._distance_dev(nd, cd, rn, rc, cfg, 0)
+    p = n.shape[0]
+    for k, r in enumerate(reps):
+        pair = ev._distance_dev(nd, cd, rn[k:k + 1].expand(p, -1, -1).contiguous(),
+                                rc[k:k + 1].expand(p, -1, -1).contiguous(), cfg, 1)  # pair kernel (Q == P)
+        one = ev._distance_dev(nd, cd, rn[k:k + 1], rc[k:k + 1], cfg, 1)           # reps kernel (Q == 1)
+        got, ref = mat[k].cpu().numpy(), pair.cpu().numpy()
+        assert np.array_equal(got, ref, equal_nan=True), r
+        assert np.array_equal(one.cpu().numpy(), ref, equal_nan=True), r
+    assert torch.isfinite(mat).any()
+
+
 @pytest.mark.parametrize("small", [8192, 0], ids=["host-bookkeeping", "device-bookkeeping"])
 def test_speciate_matches_reference(tn, monkeypatch, small):
     """Both speciation paths (host bookkeeping for small populations, device
