@@ -70,8 +70,11 @@ class Problem:
             # one read-back for fitness and per-genome status; the kernel ran
             # with capacity-sized launch bounds, so no transform read-back first
             fit, status = fused
-            host = torch.cat([fit, status.to(torch.float64)]).cpu().numpy()
-            self._check(host[stacked.size:].astype(np.int64))
+            # every status bit is an error: read back the fitness and a count of
+            # flagged genomes; the status array itself only when one is flagged
+            host = torch.cat([fit, torch.count_nonzero(status).to(torch.float64).reshape(1)]).cpu().numpy()
+            if host[stacked.size] != 0:
+                self._check(status.cpu().numpy().astype(np.int64))
             return host[:stacked.size]
         from .inference import finalize_transform
         cyclic = finalize_transform(stacked)

@@ -18,7 +18,8 @@ problem = tn.make_problem(cfg)
 root = tn.RngStream(cfg.seed)
 pop, species = state.population, state.species
 acc = {}
-for gen in range(40):
+GENS = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+for gen in range(GENS):
     rng = root.child(gen)
     t = [time.perf_counter()]
     fit = problem.evaluate_population_tensors(pop, rng=rng.child(evo.STAGE_EVAL))
@@ -33,5 +34,5 @@ for gen in range(40):
     torch.cuda.synchronize(); t.append(time.perf_counter())
     if gen >= 10:
         for k, name in enumerate(["eval", "stagnation+spawns", "reproduce", "speciate"]):
-            acc[name] = acc.get(name, 0) + (t[k + 1] - t[k]) / 30
+            acc[name] = acc.get(name, 0) + (t[k + 1] - t[k]) / max(1, GENS - 10)
 print({k: f"{1e3 * v:.3f} ms" for k, v in acc.items()}, "total", f"{1e3 * sum(acc.values()):.3f} ms")
