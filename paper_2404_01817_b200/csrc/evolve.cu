@@ -829,7 +829,9 @@ int an_distance(const double* n1, const double* c1, int64_t P, const double* n2,
   // P genomes against a few representatives: representatives staged once per
   // persistent CTA (when they fit in shared memory)
   // (in launches of as many representatives as fit in 110 KB)
-  if ((!pair_mode || Q == 1) && N < 65536 && C < 65536) {
+  // (small launches keep the warp-per-pair kernel: thread-per-pair work only
+  // fills the GPU from ~64K pairs on)
+  if ((!pair_mode || Q == 1) && P * Q >= 65536 && N < 65536 && C < 65536) {
     int64_t qc = Q < 256 ? Q : 256;
     while (qc > 1 && rep_smem_bytes((int)qc, N, C, nullptr, nullptr) > 110 * 1024) --qc;
     if (rep_smem_bytes((int)qc, N, C, nullptr, nullptr) <= 110 * 1024) {

@@ -138,11 +138,12 @@ def test_distance_representatives_kernel_equals_pairwise(tn):
     lc = np.nonzero(~np.isnan(cc[6, :, 0]))[0]
     cc[6, lc[0], 3] = np.inf
     ev = tn.evolution
-    nd, cd = ev._dev64(n), ev._dev64(cc)
+    tile = -(-65536 // n.shape[0])  # the representatives kernel runs from 64K pairs on
+    nd, cd = ev._dev64(np.tile(n, (tile, 1, 1))), ev._dev64(np.tile(cc, (tile, 1, 1)))
     reps = [0, 4, 5, 6, 9, 17, 33]
     rn, rc = nd[reps].contiguous(), cd[reps].contiguous()
     mat = ev._distance_dev(nd, cd, rn, rc, cfg, 0)
-    p = n.shape[0]
+    p = nd.shape[0]
     for k, r in enumerate(reps):
         pair = ev._distance_dev(nd, cd, rn[k:k + 1].expand(p, -1, -1).contiguous(),
                                 rc[k:k + 1].expand(p, -1, -1).contiguous(), cfg, 1)  # pair kernel (Q == P)

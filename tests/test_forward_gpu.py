@@ -265,7 +265,9 @@ def test_large_host_uploads_staged(tn):
     assert conns.nbytes > 2 * _STAGE_BYTES
     a, _ = tn.transform_arrays(nodes, conns, 32, 8)
     b, _ = tn.transform_arrays(torch.from_numpy(nodes).cuda(), torch.from_numpy(conns).cuda(), 32, 8)
-    assert torch.equal(a.program, b.program)
+    assert torch.equal(a.program[:, :32], b.program[:, :32])  # headers (the unused tails are not written)
+    xa = torch.randn(a.size, 8, 32, device="cuda")
+    assert torch.equal(tn.forward_device(a, xa), tn.forward_device(b, xa))
     sub = a.select(slice(5, 17))
     np.testing.assert_array_equal(sub._cache["slots"], a._cache["slots"][5:17])
     x = torch.randn(12, 300, 32, device="cuda")
