@@ -18,10 +18,12 @@ state = init_state(cfg)
 problem = tn.make_problem(cfg)
 root = tn.RngStream(cfg.seed)
 pop, species = state.population, state.species
-for gen in range(2):
+for gen in range(5):
     rng = root.child(gen)
     fit = problem.evaluate_population_tensors(pop, rng=rng.child(evo.STAGE_EVAL))
+    ts = time.perf_counter()
     surv = evo.update_stagnation(species, fit, cfg)
+    tu = time.perf_counter()
     alloc = evo.allocate_spawns(surv, fit, cfg)
     t0 = time.perf_counter()
     tabs = evo.slot_tables(alloc, fit, cfg)
@@ -35,5 +37,6 @@ for gen in range(2):
     pop, species = evo.speciate(off, alloc, cfg)
     torch.cuda.synchronize()
     t4 = time.perf_counter()
-    print(f"gen {gen}: slot_tables {1e3*(t1-t0):.1f} ms, reproduce total {1e3*(t3-t2):.1f} ms, "
+    print(f"gen {gen}: stagnation {1e3*(tu-ts):.1f} ms, spawns {1e3*(t0-tu):.1f} ms, "
+          f"slot_tables {1e3*(t1-t0):.1f} ms, reproduce total {1e3*(t3-t2):.1f} ms, "
           f"speciate {1e3*(t4-t3):.1f} ms, species {len(species)}", flush=True)
