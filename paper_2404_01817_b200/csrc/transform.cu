@@ -28,18 +28,69 @@ constexpr uint64_t U64_MAX = ~0ull;
 constexpr int32_t NEVER = 0x7FFFFFFF;
 constexpr uint8_t F_LIVE = 1, F_INPUT = 2, F_OUTPUT = 4, F_FREED = 8;
 
+// Edge keys (dst, src, connection row) and step sort keys (level, class,
+// -count, position), packed so that integer order is the sort order.  Genomes
+// with N <= 256 and C <= 16383 use 32-bit keys and byte successor lists: a
+// genome-warp then needs 10.7 instead of 13.7 KB of shared memory at 128/512
+// (more resident warps -- the transform is latency-bound).
+template <bool SMALL> struct KeyTraits;
+template <> struct KeyTraits<false> {
+  using E = uint64_t;
+  using G = uint64_t;
+  using Succ = uint16_t;
+  static constexpr int DSH = 48, SSH = 32;
+  static constexpr uint32_t FM = 0xFFFF;
+  static constexpr G GMAX = ~0ull;
+  __device__ static E make(int d, int s, int c) { return ((uint64_t)d << 48) | ((uint64_t)s << 32) | (uint64_t)c; }
+  __device__ static int dst(E k) { return (int)((k >> 48) & 0xFFFF); }
+  __device__ static int src(E k) { return (int)((k >> 32) & 0xFFFF); }
+  __device__ static int64_t row(E k) { return (int64_t)(k & 0xFFFFFFFFu); }
+  __device__ static bool same_pair(E a, E b) { return ((a ^ b) >> 32) == 0; }
+  __device__ static G gmake(uint32_t lv, uint32_t cls, uint32_t cnt, uint32_t pos) {
+    return ((uint64_t)lv << 48) | ((uint64_t)cls << 47) | ((uint64_t)(0xFFFF - cnt) << 16) | (uint64_t)pos;
+  }
+  __device__ static int gpos(G k) { return (int)(k & 0xFFFF); }
+  __device__ static int gcnt(G k) { return 0xFFFF - (int)((k >> 16) & 0xFFFF); }
+  __device__ static int gcls(G k) { return (int)((k >> 47) & 1); }
+  __device__ static int glv(G k) { return (int)(k >> 48); }
+};
+template <> struct KeyTraits<true> {
+  using E = uint32_t;
+  using G = uint32_t;
+  using Succ = uint8_t;
+  static constexpr int DSH = 24, SSH = 16;
+  static constexpr uint32_t FM = 0xFF;
+  static constexpr G GMAX = ~0u;
+  __device__ static E make(int d, int s, int c) { return ((uint32_t)d << 24) | ((uint32_t)s << 16) | (uint32_t)c; }
+  __device__ static int dst(E k) { return (int)((k >> 24) & 0xFF); }
+  __device__ static int src(E k) { return (int)((k >> 16) & 0xFF); }
+  __device__ static int64_t row(E k) { return (int64_t)(k & 0xFFFFu); }
+  __device__ static bool same_pair(E a, E b) { return ((a ^ b) >> 16) == 0; }
+  __device__ static G gmake(uint32_t lv, uint32_t cls, uint32_t cnt, uint32_t pos) {
+    return (lv << 24) | (cls << 23) | ((0x3FFFu - cnt) << 9) | pos;
+  }
+  __device__ static int gpos(G k) { return (int)(k & 0x1FF); }
+  __device__ static int gcnt(G k) { return 0x3FFF - (int)((k >> 9) & 0x3FFF); }
+  __device__ static int gcls(G k) { return (int)((k >> 23) & 1); }
+  __device__ static int glv(G k) { return (int)(k >> 24); }
+};
+__host__ __device__ inline bool small_keys(int N, int C) { return N <= 256 && C <= 16383; }
+
+template <typename KT>
 struct WarpSmem {
+  using E = typename KT::E;
+  using G = typename KT::G;
   uint64_t* skey;     // [Npad]   (key << 16 | row), sorted
-  uint64_t* ekey;     // [Cpad]   (dst << 48 | src << 32 | conn_row), sorted
-  uint64_t* ekey2;    // [C]      unsorted staging for the counting sort
-  uint64_t* gkey;     // [Npad]   step sort keys
+  E* ekey;            // [Cpad]   edge keys, sorted (CSR by destination)
+  E* ekey2;           // [C]      unsorted staging for the counting sort
+  G* gkey;            // [Npad]   step sort keys
   int32_t* indeg;     // [N]
   int32_t* outdeg;    // [N]
   int32_t* in_start;  // [N+1]    CSR by destination into ekey
   int32_t* su_start;  // [N+1]    CSR by source into succ
   int32_t* lvl;       // [N]      topological level
   int32_t* last_grp;  // [N+1]    last group that reads the node (level starts during Kahn)
-  uint16_t* succ;     // [C]
+  typename KT::Succ* succ;  // [C] destination rows, CSR by source
   uint16_t* order;    // [N]
   uint16_t* slot_of;  // [N]
   uint16_t* step_row; // [N]
@@ -59,8 +110,10 @@ __host__ __device__ inline int next_pow2(int x) {
   return p;
 }
 
-template <bool kCarve>
-__host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, bool split, WarpSmem* s) {
+template <bool kCarve, typename KT>
+__host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, bool split, WarpSmem<KT>* s) {
+  using E = typename KT::E;
+  using G = typename KT::G;
   const int Npad = next_pow2(N), Cpad = next_pow2(C);
   const int W = (N + 31) / 32, WS = (N + 2 + 31) / 32;
   int64_t o = 0;
@@ -70,27 +123,29 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, bool
     o += bytes;
     return at;
   };
-  const int64_t a_skey = take(8ll * Npad, 8), a_ekey = take(8ll * Cpad, 8);
+  const int64_t a_skey = take(8ll * Npad, 8), a_ekey = take((int64_t)sizeof(E) * Cpad, 8);
   // union: ekey2 (edge staging, dead once the CSR is built) shares memory with
   // the arrays that are first written after Kahn (gkey, grp, last_grp,
   // step_row, grp_of)
   const int64_t a_union = take(0, 16);
-  const int64_t a_gkey = take(8ll * Npad, 8), a_grp = take((split ? 32ll : 16ll) * N, 16);
+  const int64_t a_gkey = take((int64_t)sizeof(G) * Npad, 8), a_grp = take((split ? 32ll : 16ll) * N, 16);
   const int64_t a_last = take(4ll * (N + 1), 4);  // also the level starts of the level-synchronous Kahn
   const int64_t a_srow = take(2ll * N, 2), a_grpof = take(2ll * N, 2);
   const int64_t a_ekey2 = a_union;
-  o = a_union + (o - a_union > 8ll * (C > 0 ? C : 1) ? o - a_union : 8ll * (C > 0 ? C : 1));
+  const int64_t e2 = (int64_t)sizeof(E) * (C > 0 ? C : 1);
+  o = a_union + (o - a_union > e2 ? o - a_union : e2);
   const int64_t a_indeg = take(4ll * N, 4), a_outdeg = take(4ll * N, 4);
   const int64_t a_in = take(4ll * (N + 1), 4), a_su = take(4ll * (N + 1), 4);
   const int64_t a_lvl = take(4ll * N, 4);
-  const int64_t a_succ = take(2ll * C, 2), a_order = take(2ll * N, 2), a_slot = take(2ll * N, 2);
+  const int64_t a_succ = take((int64_t)sizeof(typename KT::Succ) * C, 2), a_order = take(2ll * N, 2),
+                a_slot = take(2ll * N, 2);
   const int64_t a_flags = take(N, 1), a_needed = take(N, 1), a_used = take(N, 1);
   const int64_t a_ready = take(4ll * W, 4), a_free = take(4ll * WS, 4);
   if (kCarve) {
     s->skey = (uint64_t*)(base + a_skey);
-    s->ekey = (uint64_t*)(base + a_ekey);
-    s->ekey2 = (uint64_t*)(base + a_ekey2);
-    s->gkey = (uint64_t*)(base + a_gkey);
+    s->ekey = (E*)(base + a_ekey);
+    s->ekey2 = (E*)(base + a_ekey2);
+    s->gkey = (G*)(base + a_gkey);
     s->indeg = (int32_t*)(base + a_indeg);
     s->outdeg = (int32_t*)(base + a_outdeg);
     s->in_start = (int32_t*)(base + a_in);
@@ -99,7 +154,7 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, bool
     s->last_grp = (int32_t*)(base + a_last);
     s->grp = (GroupRec*)(base + a_grp);
     s->grps = (GroupSplit*)(base + a_grp);
-    s->succ = (uint16_t*)(base + a_succ);
+    s->succ = (typename KT::Succ*)(base + a_succ);
     s->order = (uint16_t*)(base + a_order);
     s->slot_of = (uint16_t*)(base + a_slot);
     s->step_row = (uint16_t*)(base + a_srow);
@@ -114,18 +169,20 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, bool
 }
 
 __host__ inline int64_t warp_smem_bytes(int N, int C, bool split) {
-  return layout_warp<false>(nullptr, N, C, split, nullptr);
+  if (small_keys(N, C)) return layout_warp<false, KeyTraits<true>>(nullptr, N, C, split, nullptr);
+  return layout_warp<false, KeyTraits<false>>(nullptr, N, C, split, nullptr);
 }
 
-// ascending bitonic sort of n (power of two, >= 32) u64 values, one warp
-__device__ void warp_bitonic_sort(uint64_t* a, int n) {
+// ascending bitonic sort of n (power of two, >= 32) values, one warp
+template <typename K>
+__device__ void warp_bitonic_sort(K* a, int n) {
   const int lane = threadIdx.x & 31;
   for (int k = 2; k <= n; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = lane; i < n; i += 32) {
         const int l = i ^ j;
         if (l > i) {
-          const uint64_t x = a[i], y = a[l];
+          const K x = a[i], y = a[l];
           const bool up = (i & k) == 0;
           if ((x > y) == up) { a[i] = y; a[l] = x; }
         }
@@ -161,14 +218,15 @@ __device__ void warp_exclusive_scan(const int32_t* cnt, int32_t* out, int n) {
 // __match_any_sync and the lowest of them advances the bucket cursor.  With
 // `succ`, also writes the destination row (bits 48..63) of each key at its
 // position (the CSR by source).
-__device__ void stable_scatter(const uint64_t* in, uint64_t* out, int n, int shift, const int32_t* start,
-                               int32_t* cursor, uint16_t* succ) {
+template <typename KT>
+__device__ void stable_scatter(const typename KT::E* in, typename KT::E* out, int n, int shift,
+                               const int32_t* start, int32_t* cursor, typename KT::Succ* succ) {
   const int lane = threadIdx.x & 31;
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
     const bool valid = i < n;
-    const uint64_t k = valid ? in[i] : 0ull;
-    const uint32_t b = valid ? (uint32_t)((k >> shift) & 0xFFFF) : 0xFFFFFFFFu;
+    const typename KT::E k = valid ? in[i] : 0;
+    const uint32_t b = valid ? (uint32_t)((k >> shift) & KT::FM) : 0xFFFFFFFFu;
     const unsigned peers = __match_any_sync(0xffffffffu, b);
     const int leader = __ffs(peers) - 1;
     int old = 0;
@@ -180,7 +238,7 @@ __device__ void stable_scatter(const uint64_t* in, uint64_t* out, int n, int shi
     if (valid) {
       const int pos = start[b] + old + __popc(peers & ((1u << lane) - 1));
       out[pos] = k;
-      if (succ) succ[pos] = (uint16_t)((k >> 48) & 0xFFFF);
+      if (succ) succ[pos] = (typename KT::Succ)KT::dst(k);
     }
     __syncwarp();
   }
@@ -212,7 +270,7 @@ __device__ inline int warp_first_set(const uint32_t* words, int nw) {
   return (int)wmin * 32 + __ffs(words[wmin]) - 1;
 }
 
-template <typename T>
+template <typename T, bool SMALL>
 __global__ void transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
                                  int64_t P, int N, int C, int I, int O, int mode, int prune, bool split,
                                  int64_t wsmem, uint8_t* __restrict__ prog, ProgLayout L,
@@ -224,8 +282,9 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   const int warp = threadIdx.x >> 5;
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (g >= P) return;
-  WarpSmem s;
-  layout_warp<true>(smem + warp * wsmem, N, C, split, &s);
+  using KT = KeyTraits<SMALL>;
+  WarpSmem<KT> s;
+  layout_warp<true, KT>(smem + warp * wsmem, N, C, split, &s);
   const int Npad = next_pow2(N);
   const double* gn = nodes + g * (int64_t)N * 5;
   const double* gc = conns + g * (int64_t)C * 4;
@@ -293,7 +352,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     const unsigned m = __ballot_sync(0xffffffffu, en);
     if (en) {
       const int pos = n_en + __popc(m & ((1u << lane) - 1));
-      s.ekey2[pos] = ((uint64_t)dr << 48) | ((uint64_t)sr << 32) | (uint64_t)c;
+      s.ekey2[pos] = KT::make(dr, sr, c);
     }
     n_en += __popc(m);
   }
@@ -302,9 +361,9 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   // ---- counting sort by destination, then by source inside each bucket; CSR by
   // destination (in_start) and by source (su_start/succ) ------------------------
   for (int e = lane; e < n_en; e += 32) {
-    const uint64_t k = s.ekey2[e];
-    atomicAdd(&s.indeg[(int)((k >> 48) & 0xFFFF)], 1);
-    atomicAdd(&s.outdeg[(int)((k >> 32) & 0xFFFF)], 1);
+    const typename KT::E k = s.ekey2[e];
+    atomicAdd(&s.indeg[KT::dst(k)], 1);
+    atomicAdd(&s.outdeg[KT::src(k)], 1);
   }
   __syncwarp();
   warp_exclusive_scan(s.indeg, s.in_start, N);
@@ -314,8 +373,8 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   // two stable, order-preserving scatters (LSD radix by source, then by
   // destination): the edges start in connection-row order, so every
   // destination bucket ends up sorted by (source row, connection row)
-  stable_scatter(s.ekey2, s.ekey, n_en, 32, s.su_start, s.outdeg, s.succ);
-  stable_scatter(s.ekey, s.ekey2, n_en, 48, s.in_start, s.lvl, nullptr);
+  stable_scatter<KT>(s.ekey2, s.ekey, n_en, KT::SSH, s.su_start, s.outdeg, s.succ);
+  stable_scatter<KT>(s.ekey, s.ekey2, n_en, KT::DSH, s.in_start, s.lvl, nullptr);
   for (int e = lane; e < n_en; e += 32) s.ekey[e] = s.ekey2[e];
   __syncwarp();
   int shadowed_any = 0;
@@ -326,11 +385,11 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     // shadowed -- counted here, removed below
     int kept = 0;
     for (int i = b0; i < b1; ++i) {
-      const bool shadow = i + 1 < b1 && ((s.ekey[i] ^ s.ekey[i + 1]) >> 32) == 0;
+      const bool shadow = i + 1 < b1 && KT::same_pair(s.ekey[i], s.ekey[i + 1]);
       if (shadow) {
         ++shadowed_any;
-        if (conn_rows) conn_rows[(g * C + (int64_t)(s.ekey[i] & 0xFFFFFFFFu)) * 2 + 0] = -1,
-                       conn_rows[(g * C + (int64_t)(s.ekey[i] & 0xFFFFFFFFu)) * 2 + 1] = -1;
+        if (conn_rows) conn_rows[(g * C + KT::row(s.ekey[i])) * 2 + 0] = -1,
+                       conn_rows[(g * C + KT::row(s.ekey[i])) * 2 + 1] = -1;
       } else {
         ++kept;
       }
@@ -367,7 +426,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       for (int r = lane; r < N; r += 32) {
         int at = s.outdeg[r];
         for (int i = s.in_start[r]; i < s.in_start[r + 1]; ++i)
-          if (!(i + 1 < s.in_start[r + 1] && ((s.ekey[i] ^ s.ekey[i + 1]) >> 32) == 0)) s.ekey2[at++] = s.ekey[i];
+          if (!(i + 1 < s.in_start[r + 1] && KT::same_pair(s.ekey[i], s.ekey[i + 1]))) s.ekey2[at++] = s.ekey[i];
       }
       __syncwarp();
       for (int i = lane; i < carry; i += 32) s.ekey[i] = s.ekey2[i];
@@ -489,7 +548,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
         const int r = s.order[i];
         if (!s.needed[r] || (s.flags[r] & F_INPUT)) continue;
         for (int e = s.in_start[r]; e < s.in_start[r + 1]; ++e) {
-          const int sr = (int)((s.ekey[e] >> 32) & 0xFFFF);
+          const int sr = KT::src(s.ekey[e]);
           s.needed[sr] = 1;
           s.used[sr] = 1;
         }
@@ -504,7 +563,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       const int r = s.order[i];
       if (!s.needed[r] || (s.flags[r] & F_INPUT)) continue;
       for (int e = s.in_start[r] + lane; e < s.in_start[r + 1]; e += 32) {
-        const int sr = (int)((s.ekey[e] >> 32) & 0xFFFF);
+        const int sr = KT::src(s.ekey[e]);
         s.needed[sr] = 1;
         s.used[sr] = 1;
       }
@@ -535,24 +594,23 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       if (!(av >= 0.0 && av < ACT_COUNT && av == floor(av))) bad |= ST_BAD_ACT;
       if (!(gv >= 0.0 && gv < AGG_COUNT && gv == floor(gv))) bad |= ST_BAD_AGG;
       const int agg = (gv >= 0.0 && gv < AGG_COUNT) ? (int)gv : 0;
-      const uint64_t cls = (recurrent || !(agg == AGG_SUM || agg == AGG_MEAN)) ? 1 : 0;
-      uint64_t cnt = (uint64_t)(s.in_start[r + 1] - s.in_start[r]);
+      const uint32_t cls = (recurrent || !(agg == AGG_SUM || agg == AGG_MEAN)) ? 1 : 0;
+      uint32_t cnt = (uint32_t)(s.in_start[r + 1] - s.in_start[r]);
       if (split) {  // split programs group by the input-edge count (outdeg: free since the CSR build)
         int cin = 0;
         for (int e = s.in_start[r]; e < s.in_start[r + 1]; ++e)
-          cin += (s.flags[(int)((s.ekey[e] >> 32) & 0xFFFF)] & F_INPUT) ? 1 : 0;
+          cin += (s.flags[KT::src(s.ekey[e])] & F_INPUT) ? 1 : 0;
         s.outdeg[r] = cin;
-        cnt = (uint64_t)cin;
+        cnt = (uint32_t)cin;
       }
-      const uint64_t lv = recurrent ? 0 : (uint64_t)s.lvl[r];
-      s.gkey[n_emit + __popc(me & ((1u << lane) - 1))] =
-          (lv << 48) | (cls << 47) | ((0xFFFFull - cnt) << 16) | (uint64_t)i;
+      const uint32_t lv = recurrent ? 0 : (uint32_t)s.lvl[r];
+      s.gkey[n_emit + __popc(me & ((1u << lane) - 1))] = KT::gmake(lv, cls, cnt, (uint32_t)i);
     }
     n_emit += __popc(me);
   }
   status |= __reduce_or_sync(0xffffffffu, bad);
   const int Spad = next_pow2(n_emit);
-  for (int i = n_emit + lane; i < Spad; i += 32) s.gkey[i] = U64_MAX;
+  for (int i = n_emit + lane; i < Spad; i += 32) s.gkey[i] = KT::GMAX;
   __syncwarp();
   warp_bitonic_sort(s.gkey, Spad);
 
@@ -576,13 +634,13 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       e_total = (int)align_up(e_total + gw * gr.rounds_h, 8);
     };
     for (int k = 0; k < n_emit; ++k) {
-      const uint64_t key = s.gkey[k];
-      const int pos = (int)(key & 0xFFFF);
+      const typename KT::G key = s.gkey[k];
+      const int pos = KT::gpos(key);
       const int row = (int)s.order[pos];
-      const int cin = 0xFFFF - (int)((key >> 16) & 0xFFFF);
+      const int cin = KT::gcnt(key);
       const int ch = s.in_start[row + 1] - s.in_start[row] - cin;
-      const int cls = (int)((key >> 47) & 1);
-      const int lv = (int)(key >> 48);
+      const int cls = KT::gcls(key);
+      const int lv = KT::glv(key);
       const bool join = ng > 0 && lv == cur_lv && cls == cur_cls && cls == 0 && s.grps[ng - 1].n < 4 &&
                         TNEAT_JOIN_DEN * cin >= TNEAT_JOIN_NUM * cur_rounds;
       if (!join) {
@@ -613,12 +671,12 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     int ng = 0, e_total = 0;
     int cur_lv = -1, cur_cls = -1, cur_rounds = 0;
     for (int k = 0; k < n_emit; ++k) {
-      const uint64_t key = s.gkey[k];
-      const int pos = (int)(key & 0xFFFF);
+      const typename KT::G key = s.gkey[k];
+      const int pos = KT::gpos(key);
       const int row = recurrent ? pos : (int)s.order[pos];
-      const int cnt = 0xFFFF - (int)((key >> 16) & 0xFFFF);
-      const int cls = (int)((key >> 47) & 1);
-      const int lv = (int)(key >> 48);
+      const int cnt = KT::gcnt(key);
+      const int cls = KT::gcls(key);
+      const int lv = KT::glv(key);
       const bool join = ng > 0 && lv == cur_lv && cls == cur_cls && cls == 0 && s.grp[ng - 1].n < 4 &&
                         TNEAT_JOIN_DEN * cnt >= TNEAT_JOIN_NUM * cur_rounds;
       if (!join) {
@@ -657,7 +715,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       const int row = s.step_row[k];
       const int gk = s.grp_of[k];
       for (int e = s.in_start[row]; e < s.in_start[row + 1]; ++e)
-        atomicMax(&s.last_grp[(int)((s.ekey[e] >> 32) & 0xFFFF)], gk);
+        atomicMax(&s.last_grp[KT::src(s.ekey[e])], gk);
     }
   }
   // slots: 0..I-1 hold the inputs, the rest start free; one more slot after
@@ -745,9 +803,9 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       }
       int ri = 0, rh = 0;  // source-row order inside each block
       for (int e = e0; e < e0 + cnt; ++e) {
-        const uint64_t kk = s.ekey[e];
-        const int sr = (int)((kk >> 32) & 0xFFFF);
-        const float w = (float)gc[(int64_t)(kk & 0xFFFFFFFFu) * 4 + 3];
+        const typename KT::E kk = s.ekey[e];
+        const int sr = KT::src(kk);
+        const float w = (float)gc[KT::row(kk) * 4 + 3];
         if (s.flags[sr] & F_INPUT) {
           const int idx = gr.e_in + (ri++) * gw + j;
           esrc[idx] = (uint16_t)gn[(int64_t)sr * 5];
@@ -788,9 +846,9 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
         uint32_t src = zero_slot;
         double w = 0.0;
         if (col == j && rr < cnt) {
-          const uint64_t kk = s.ekey[e0 + rr];
-          src = s.slot_of[(int)((kk >> 32) & 0xFFFF)];
-          w = gc[(int64_t)(kk & 0xFFFFFFFFu) * 4 + 3];
+          const typename KT::E kk = s.ekey[e0 + rr];
+          src = s.slot_of[KT::src(kk)];
+          w = gc[KT::row(kk) * 4 + 3];
         }
         if (sizeof(T) == 8) {
           EdgeD ed;
@@ -845,21 +903,27 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
   const int Cc = C > 0 ? C : 1;
   const int64_t ws = warp_smem_bytes(N, Cc, split);
   if (ws > 200 * 1024) return -4;  // genome capacity too large for one warp's shared memory
-  int wpb = 4;
+#ifndef TNEAT_TR_WPB
+#define TNEAT_TR_WPB 1  // one genome-warp per CTA: its shared memory is released as soon as it finishes
+#endif
+  int wpb = TNEAT_TR_WPB;
   while (wpb > 1 && ws * wpb > 160 * 1024) wpb >>= 1;
   const int64_t smem = ws * wpb;
   const int64_t blocks = (P + wpb - 1) / wpb;
   cudaStream_t st = (cudaStream_t)stream;
+  auto launch = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel<<<(unsigned)blocks, 32 * wpb, smem, st>>>(nodes, conns, P, N, C, I, O, mode, prune, split, ws,
+                                                     (uint8_t*)program, L, order, conn_rows, io_rows, status,
+                                                     maxdims);
+  };
+  const bool small = small_keys(N, Cc);
   if (precision & FMT_F64) {
-    cudaFuncSetAttribute(transform_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    transform_kernel<double><<<(unsigned)blocks, 32 * wpb, smem, st>>>(
-        nodes, conns, P, N, C, I, O, mode, prune, split, ws, (uint8_t*)program, L, order, conn_rows,
-        io_rows, status, maxdims);
+    if (small) launch(transform_kernel<double, true>);
+    else launch(transform_kernel<double, false>);
   } else {
-    cudaFuncSetAttribute(transform_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    transform_kernel<float><<<(unsigned)blocks, 32 * wpb, smem, st>>>(
-        nodes, conns, P, N, C, I, O, mode, prune, split, ws, (uint8_t*)program, L, order, conn_rows,
-        io_rows, status, maxdims);
+    if (small) launch(transform_kernel<float, true>);
+    else launch(transform_kernel<float, false>);
   }
   TNEAT_CHECK_LAUNCH();
   return 0;
