@@ -8,6 +8,9 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2404_01817_b200 as tn  # noqa: E402
+if os.environ.get("TNEAT_TOOL_LIB"):  # A/B of a tools/build_variant.py library
+    from paper_2404_01817_b200 import _native  # noqa: E402
+    _native.LIB_PATH = os.path.abspath(os.environ["TNEAT_TOOL_LIB"])
 from paper_2404_01817_b200 import evolution as evo  # noqa: E402
 from paper_2404_01817_b200.runner import init_state  # noqa: E402
 
