@@ -179,13 +179,12 @@ __device__ void warp_bitonic_sort(K* a, int n) {
   const int lane = threadIdx.x & 31;
   for (int k = 2; k <= n; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = lane; i < n; i += 32) {
-        const int l = i ^ j;
-        if (l > i) {
-          const K x = a[i], y = a[l];
-          const bool up = (i & k) == 0;
-          if ((x > y) == up) { a[i] = y; a[l] = x; }
-        }
+      for (int t = lane; t < (n >> 1); t += 32) {  // compare-exchange pair t: (i, i + j)
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int l = i + j;
+        const K x = a[i], y = a[l];
+        const bool up = (i & k) == 0;
+        if ((x > y) == up) { a[i] = y; a[l] = x; }
       }
       __syncwarp();
     }
@@ -244,15 +243,15 @@ __device__ void stable_scatter(const typename KT::E* in, typename KT::E* out, in
   }
 }
 
-// row of `key` among the sorted live (key<<16|row) pairs, or -1
+// row of `key` among the sorted live (key<<16|row) pairs, or -1: branchless
+// search over the power-of-two table (packed entries compare against key<<16
+// directly, keys < 2^47); the smallest row wins for a repeated key
 __device__ inline int lookup_row(const uint64_t* skey, int Npad, uint64_t key) {
-  int lo = 0, hi = Npad;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if ((skey[mid] >> 16) < key) lo = mid + 1; else hi = mid;
-  }
-  if (lo < Npad && skey[lo] != U64_MAX && (skey[lo] >> 16) == key) return (int)(skey[lo] & 0xFFFF);
-  return -1;
+  const uint64_t kk = key << 16;
+  int pos = 0;
+  for (int step = Npad >> 1; step > 0; step >>= 1) pos = skey[pos + step - 1] < kk ? pos + step : pos;
+  const uint64_t e = skey[pos];
+  return (e != U64_MAX && (e >> 16) == key) ? (int)(e & 0xFFFF) : -1;
 }
 
 __device__ inline bool key_ok(double k) {
