@@ -26,7 +26,7 @@ constexpr uint64_t U64_MAX = ~0ull;
 #define TNEAT_JOIN_DEN 2
 #endif
 constexpr int32_t NEVER = 0x7FFFFFFF;
-constexpr uint8_t F_LIVE = 1, F_INPUT = 2, F_OUTPUT = 4, F_FREED = 8;
+constexpr uint8_t F_LIVE = 1, F_INPUT = 2, F_OUTPUT = 4, F_FREED = 8, F_TANH_SUM = 16;
 
 // Edge keys (dst, src, connection row) and step sort keys (level, class,
 // -count, position), packed so that integer order is the sort order.  Genomes
@@ -308,6 +308,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
           const double av = gn[(int64_t)r * 5 + 4], gv = gn[(int64_t)r * 5 + 3];
           if (!(av >= 0.0 && av < ACT_COUNT && av == floor(av))) status |= ST_BAD_ACT;
           if (!(gv >= 0.0 && gv < AGG_COUNT && gv == floor(gv))) status |= ST_BAD_AGG;
+          if (av == (double)ACT_TANH && gv == (double)AGG_SUM) f |= F_TANH_SUM;  // read by the group pass
         }
       }
       s.flags[r] = f;
@@ -656,7 +657,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       gr.cnt_in[gr.n] = (uint16_t)cin;
       gr.cnt_h[gr.n] = (uint16_t)ch;
       if (ch > gr.rounds_h) gr.rounds_h = (uint16_t)ch;
-      const bool tanh_sum = gn[(int64_t)row * 5 + 4] == (double)ACT_TANH && gn[(int64_t)row * 5 + 3] == (double)AGG_SUM;
+      const bool tanh_sum = (s.flags[row] & F_TANH_SUM) != 0;
       if (gr.n == 0) gr.cls |= tanh_sum ? GRP_TANH_SUM : 0;
       else if (!tanh_sum) gr.cls &= ~GRP_TANH_SUM;
       gr.n++;
@@ -690,7 +691,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       }
       GroupRec& gr = s.grp[ng - 1];
       gr.cnt[gr.n] = (uint16_t)cnt;
-      const bool tanh_sum = gn[(int64_t)row * 5 + 4] == (double)ACT_TANH && gn[(int64_t)row * 5 + 3] == (double)AGG_SUM;
+      const bool tanh_sum = (s.flags[row] & F_TANH_SUM) != 0;
       if (gr.n == 0) gr.cls |= tanh_sum ? GRP_TANH_SUM : 0;
       else if (!tanh_sum) gr.cls &= ~GRP_TANH_SUM;
       gr.n++;
