@@ -841,22 +841,34 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     // 3-group) are (zero slot, 0.0) entries
     const int ncol = (gr.n == 3 && j == 2) ? 2 : 1;
     for (int col = j; col < j + ncol; ++col) {
-      for (int rr = 0; rr < gr.rounds; ++rr) {
-        const int idx = gr.e_begin + rr * gw + col;
-        uint32_t src = zero_slot;
-        double w = 0.0;
-        if (col == j && rr < cnt) {
-          const typename KT::E kk = s.ekey[e0 + rr];
-          src = s.slot_of[KT::src(kk)];
-          w = gc[KT::row(kk) * 4 + 3];
+      // rounds in batches of 4: the weight loads of a batch are in flight together
+      for (int rr0 = 0; rr0 < gr.rounds; rr0 += 4) {
+        uint32_t src[4];
+        double w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int rr = rr0 + u;
+          src[u] = zero_slot;
+          w[u] = 0.0;
+          if (col == j && rr < cnt) {
+            const typename KT::E kk = s.ekey[e0 + rr];
+            src[u] = s.slot_of[KT::src(kk)];
+            w[u] = gc[KT::row(kk) * 4 + 3];
+          }
         }
-        if (sizeof(T) == 8) {
-          EdgeD ed;
-          ed.src = src; ed.pad = 0; ed.w = w;
-          ((EdgeD*)(gp + L.off_w))[idx] = ed;
-        } else {
-          ((uint16_t*)(gp + L.off_src))[idx] = (uint16_t)src;
-          ((float*)(gp + L.off_w))[idx] = (float)w;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int rr = rr0 + u;
+          if (rr >= gr.rounds) break;
+          const int idx = gr.e_begin + rr * gw + col;
+          if (sizeof(T) == 8) {
+            EdgeD ed;
+            ed.src = src[u]; ed.pad = 0; ed.w = w[u];
+            ((EdgeD*)(gp + L.off_w))[idx] = ed;
+          } else {
+            ((uint16_t*)(gp + L.off_src))[idx] = (uint16_t)src[u];
+            ((float*)(gp + L.off_w))[idx] = (float)w[u];
+          }
         }
       }
     }
