@@ -158,15 +158,14 @@ def run_bench(config: NeatConfig, pop_sizes: list[int], generations: int, out_di
     the same seeds), else left empty."""
     out = Path(out_dir)
     out.mkdir(parents=True, exist_ok=True)
-    # one untimed generation first: module loading and first-launch costs stay
-    # out of the smallest population's column
-    _gpu_generation_times(config.with_overrides(pop_size=max(min(pop_sizes), 2 * config.species_elitism),
-                                                generation_limit=1, fitness_target=math.inf), 1)
     rows = []
     for pop_size in pop_sizes:
         cfg = config.with_overrides(pop_size=pop_size, generation_limit=generations, fitness_target=math.inf)
         if log:
             log(f"pop_size={pop_size}: gpu path")
+        # one untimed generation per size: first-launch costs and the GPU's clock
+        # ramp after the (long) host-side reference runs stay out of the timings
+        _gpu_generation_times(cfg.with_overrides(generation_limit=1), 1)
         gpu = _gpu_generation_times(cfg, generations)
         tens = seq = [None] * generations
         if reference is not None:
