@@ -296,7 +296,46 @@ __device__ __forceinline__ void run_sum_group_f64(const GroupRec& gr, const Edge
   for (int j = 0; j < G; ++j) finish_step<S, RB>(st[j], acc[j], vb);
 }
 
-// singleton group with a non-sum aggregation (product / max / min), exact count
+// singleton group with a non-sum aggregation (product / max / min), exact
+// count; the aggregation is a template parameter (no per-edge dispatch) and the
+// edges go two at a time (both value loads in flight before the combines)
+template <typename T, int AGG>
+__device__ __forceinline__ T agg_step(T acc, T x) {
+  if constexpr (AGG == AGG_PRODUCT) return acc * x;
+  else if constexpr (AGG == AGG_MAX) return acc > x ? acc : x;
+  else if constexpr (AGG == AGG_MIN) return acc < x ? acc : x;
+  else return acc + x;
+}
+
+template <typename T, int S, int RB, int AGG>
+__device__ __forceinline__ void generic_edges(T (&acc)[S], int e_begin, int count, const uint32_t* __restrict__ off_s,
+                                              const float* __restrict__ w_s, const EdgeD* __restrict__ ed_s,
+                                              const char* vb) {
+  auto edge = [&](int e, uint32_t& off, T& w) {
+    if constexpr (sizeof(T) == 8) { off = ed_s[e_begin + e].src * RB; w = ed_s[e_begin + e].w; }
+    else { off = off_s[e_begin + e]; w = w_s[e_begin + e]; }
+  };
+  int e = 0;
+  for (; e + 2 <= count; e += 2) {
+    uint32_t o0, o1;
+    T w0, w1;
+    edge(e, o0, w0);
+    edge(e + 1, o1, w1);
+    const Pack<T, S> v0 = *reinterpret_cast<const Pack<T, S>*>(vb + o0);
+    const Pack<T, S> v1 = *reinterpret_cast<const Pack<T, S>*>(vb + o1);
+#pragma unroll
+    for (int s = 0; s < S; ++s) acc[s] = agg_step<T, AGG>(agg_step<T, AGG>(acc[s], w0 * v0.v[s]), w1 * v1.v[s]);
+  }
+  if (e < count) {
+    uint32_t o0;
+    T w0;
+    edge(e, o0, w0);
+    const Pack<T, S> v0 = *reinterpret_cast<const Pack<T, S>*>(vb + o0);
+#pragma unroll
+    for (int s = 0; s < S; ++s) acc[s] = agg_step<T, AGG>(acc[s], w0 * v0.v[s]);
+  }
+}
+
 template <typename T, int S, int RB>
 __device__ __forceinline__ void run_generic_step(const GroupRec& gr, const uint32_t* __restrict__ off_s,
                                                  const float* __restrict__ w_s, const EdgeD* __restrict__ ed_s,
@@ -305,14 +344,11 @@ __device__ __forceinline__ void run_generic_step(const GroupRec& gr, const uint3
   const T neutral = agg_neutral<T>(st.agg);
 #pragma unroll
   for (int s = 0; s < S; ++s) acc[s] = neutral;
-  for (int e = 0; e < st.count; ++e) {
-    uint32_t off;  // byte offset of the source slot in the thread's value column
-    T w;
-    if constexpr (sizeof(T) == 8) { off = ed_s[gr.e_begin + e].src * RB; w = ed_s[gr.e_begin + e].w; }
-    else { off = off_s[gr.e_begin + e]; w = w_s[gr.e_begin + e]; }
-    const Pack<T, S> v = *reinterpret_cast<const Pack<T, S>*>(vb + off);
-#pragma unroll
-    for (int s = 0; s < S; ++s) acc[s] = agg_combine<T>(st.agg, acc[s], w * v.v[s]);
+  switch (st.agg) {
+    case AGG_PRODUCT: generic_edges<T, S, RB, AGG_PRODUCT>(acc, gr.e_begin, st.count, off_s, w_s, ed_s, vb); break;
+    case AGG_MAX: generic_edges<T, S, RB, AGG_MAX>(acc, gr.e_begin, st.count, off_s, w_s, ed_s, vb); break;
+    case AGG_MIN: generic_edges<T, S, RB, AGG_MIN>(acc, gr.e_begin, st.count, off_s, w_s, ed_s, vb); break;
+    default: generic_edges<T, S, RB, AGG_SUM>(acc, gr.e_begin, st.count, off_s, w_s, ed_s, vb); break;
   }
   if (st.count == 0) {
 #pragma unroll
