@@ -207,6 +207,8 @@ def run_reference(args, rank: int) -> None:
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * POP * BATCH / value, "higher_is_better": True,
+            "step_note": (f"ms_per_step = one full {POP}-genome x {BATCH}-input step at the measured rate; each "
+                          f"timed step runs a bounded sample for ~{per_step:.0f} s (cpu_baseline.sample)"),
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(CONFIG, parallelism="host threads"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": rates[0]["kind"],
