@@ -17,6 +17,9 @@ import numpy as np
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
+if os.environ.get("TNEAT_TOOL_LIB"):  # A/B of a tools/build_variant.py library
+    from paper_2404_01817_b200 import _native  # noqa: E402
+    _native.LIB_PATH = os.path.abspath(os.environ["TNEAT_TOOL_LIB"])
 
 
 def _sync():
