@@ -352,6 +352,7 @@ def _bucket_plan(stacked: StackedNetworks, variant: int) -> list:
     # no stream sync (plans are made inside copy/compute pipelines); launches wait on the upload's event
     ids, ev = upload_async(order, stacked.program.device)
     stacked._cache[("plan_ready", variant)] = ev
+    stacked._cache[("plan_ids", variant)] = ids
     _, ms, me = stacked.maxdims
     prog = 32 * ms + (16 * me if stacked.precision & FMT_F64 else 8 * me + 16) + 16
     if variant == V_SPLIT:  # fwd_split_kernel: 4 warps, 256 inputs per tile, hidden slots only
@@ -408,7 +409,10 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
     v &= 0xF
     if (v in _TILE_TT or v == V_SPLIT) and bucketed and pop > 1:
         plan = _bucket_plan(stacked, v)
-        (stream or torch.cuda.current_stream()).wait_event(stacked._cache[("plan_ready", v)])
+        launch = stream or torch.cuda.current_stream()
+        launch.wait_event(stacked._cache[("plan_ready", v)])
+        if launch != torch.cuda.current_stream():
+            stacked._cache[("plan_ids", v)].record_stream(launch)  # allocated on the current stream
         for ids, md in plan:
             _native.call("an_forward", *args, _maxdims_arg(stacked, md), ptr(ids), ptr(inputs), gstride,
                          int(ids.numel()), *tail)
