@@ -68,7 +68,10 @@ struct __align__(16) GroupRec {  // 16 bytes
   uint16_t cnt[4];     // edge count of each step
 };
 
-enum : uint8_t { GRP_GENERIC = 1, GRP_TANH_SUM = 2 };
+// GRP_SPLIT0 (sum/mean groups of 3): the spare fourth column holds the second
+// half of step 0's list (cnt[0] = first-half count, cnt[3] = the rest;
+// StepT::count stays the total), so the group runs max(ceil(c0/2), c1) rounds
+enum : uint8_t { GRP_GENERIC = 1, GRP_TANH_SUM = 2, GRP_SPLIT0 = 4 };
 
 __host__ __device__ inline int group_width(int n) { return n == 3 ? 4 : n; }
 

@@ -176,12 +176,15 @@ __device__ __forceinline__ void sum_round1(float2 (&acc)[G][(S + 1) / 2], const 
 // are in flight (the look-ahead past the block's end stays inside shared
 // memory: weights and value slots follow the offsets).  TANH: every step is
 // tanh/sum (short epilogue).
-template <int S, int G, int RB, bool TANH>
+// MERGE (GRP_SPLIT0 groups of 3 steps): G = 4 columns, column 3 continues
+// step 0 and is added into it before the epilogue
+template <int S, int G, int RB, bool TANH, bool MERGE = false>
 __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t* __restrict__ off_s,
                                               const float* __restrict__ w_s,
                                               const StepT<float>* __restrict__ st, char* vb,
                                               const Words* pre = nullptr) {
   constexpr int GW = G == 3 ? 4 : G;
+  constexpr int NS = MERGE ? G - 1 : G;  // steps
   constexpr int SP = (S + 1) / 2;  // sample pairs: Blackwell packed fp32 (FFMA2 / FADD2)
   using PackT = Pack<float, S>;
   float2 acc[G][SP];
@@ -195,7 +198,7 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
   if constexpr (TANH) {
     constexpr float K = -2.8853900817779268f;
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
+    for (int j = 0; j < NS; ++j) {
       const StepT<float> sj = st[j];
       slot_j[j] = sj.slot;
       rk_j[j] = sj.resp * K;
@@ -233,11 +236,15 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
     load_f32<2 * GW>(wp + (r + 4) * GW, wa);
     sum_rounds<S, G, GW>(acc, ob, wb, vb);
   }
+  if constexpr (MERGE) {
+#pragma unroll
+    for (int p = 0; p < SP; ++p) acc[0][p] = __fadd2_rn(acc[0][p], acc[G - 1][p]);
+  }
   if constexpr (TANH) {
     // tanh(b + r*a) = 2 / (1 + 2^(k (b + r*a))) - 1, k = -2 log2(e): one FFMA into
     // EX2 (k folded into b and r once per step), FADD, RCP, FFMA -- |err| <~ 2e-7
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
+    for (int j = 0; j < NS; ++j) {
       const float rk = rk_j[j], bk = bk_j[j];
       PackT y;
       if constexpr (S == 1) {
@@ -261,7 +268,7 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
+    for (int j = 0; j < NS; ++j) {
       float a[S];
 #pragma unroll
       for (int s = 0; s < S; ++s) a[s] = (s & 1) ? acc[j][s / 2].y : acc[j][s / 2].x;
@@ -289,6 +296,16 @@ __device__ __forceinline__ void run_sum_group_f64(const GroupRec& gr, const Edge
         const Pack<double, S> v = *reinterpret_cast<const Pack<double, S>*>(vb + d.src * RB);
 #pragma unroll
         for (int s = 0; s < S; ++s) acc[j][s] = fma(d.w, v.v[s], acc[j][s]);
+      }
+    }
+  }
+  if constexpr (G == 3) {
+    if (gr.cls & GRP_SPLIT0) {  // step 0's second half (column 3), after its first: the list order
+      for (int r = 0; r < gr.cnt[3]; ++r) {
+        const EdgeD d = ep[r * GW + 3];
+        const Pack<double, S> v = *reinterpret_cast<const Pack<double, S>*>(vb + d.src * RB);
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[0][s] = fma(d.w, v.v[s], acc[0][s]);
       }
     }
   }
@@ -369,14 +386,20 @@ __device__ __forceinline__ void run_group(const GroupRec& gr, const uint32_t* sr
         switch (gr.n) {
           case 1: run_sum_group<S, 1, RB, true>(gr, src_s, w_s, st, vb, pre); break;
           case 2: run_sum_group<S, 2, RB, true>(gr, src_s, w_s, st, vb, pre); break;
-          case 3: run_sum_group<S, 3, RB, true>(gr, src_s, w_s, st, vb, pre); break;
+          case 3:
+            if (gr.cls & GRP_SPLIT0) run_sum_group<S, 4, RB, true, true>(gr, src_s, w_s, st, vb, pre);
+            else run_sum_group<S, 3, RB, true>(gr, src_s, w_s, st, vb, pre);
+            break;
           default: run_sum_group<S, 4, RB, true>(gr, src_s, w_s, st, vb, pre); break;
         }
       } else {
         switch (gr.n) {
           case 1: run_sum_group<S, 1, RB, false>(gr, src_s, w_s, st, vb, pre); break;
           case 2: run_sum_group<S, 2, RB, false>(gr, src_s, w_s, st, vb, pre); break;
-          case 3: run_sum_group<S, 3, RB, false>(gr, src_s, w_s, st, vb, pre); break;
+          case 3:
+            if (gr.cls & GRP_SPLIT0) run_sum_group<S, 4, RB, false, true>(gr, src_s, w_s, st, vb, pre);
+            else run_sum_group<S, 3, RB, false>(gr, src_s, w_s, st, vb, pre);
+            break;
           default: run_sum_group<S, 4, RB, false>(gr, src_s, w_s, st, vb, pre); break;
         }
       }
@@ -1048,8 +1071,9 @@ __global__ void fwd_warp_kernel(const uint8_t* __restrict__ prog, ProgLayout L, 
         const int agg = st.agg;
         const int stride = (gr.cls & GRP_GENERIC) ? 1 : gw;
         T part = agg_neutral<T>(agg);
+        const int h0 = (j == 0 && (gr.cls & GRP_SPLIT0)) ? gr.cnt[0] : 0x7FFFFFFF;  // split step 0
         for (int e = lane; e < st.count; e += 32) {
-          const int idx = gr.e_begin + e * stride + j;
+          const int idx = e < h0 ? gr.e_begin + e * stride + j : gr.e_begin + (e - h0) * stride + 3;
           uint32_t src;
           T w;
           if constexpr (sizeof(T) == 8) { src = ed[idx].src; w = ed[idx].w; }
@@ -1121,8 +1145,9 @@ __device__ void warp_eval_single(const uint8_t* gp, const ProgLayout& L, T* vals
     for (int j = 0; j < gr.n; ++j) {
       const StepT<T> st = steps[gr.step_begin + j];
       T part = agg_neutral<T>(st.agg);
+      const int h0 = (j == 0 && (gr.cls & GRP_SPLIT0)) ? gr.cnt[0] : 0x7FFFFFFF;  // split step 0
       for (int e = lane; e < st.count; e += 32) {
-        const int idx = gr.e_begin + e * stride + j;
+        const int idx = e < h0 ? gr.e_begin + e * stride + j : gr.e_begin + (e - h0) * stride + 3;
         uint32_t src;
         T w;
         if constexpr (sizeof(T) == 8) { src = ed[idx].src; w = ed[idx].w; }

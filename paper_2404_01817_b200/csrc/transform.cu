@@ -670,6 +670,21 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   } else if (lane == 0) {
     int ng = 0, e_total = 0;
     int cur_lv = -1, cur_cls = -1, cur_rounds = 0;
+    // a sum group of 3 whose first list is the longest gives the spare column
+    // to the second half of that list (GRP_SPLIT0; fp32 and fp64 programs)
+    auto close = [&](GroupRec& gr) {
+      if (gr.n == 3 && !(gr.cls & GRP_GENERIC) && !recurrent) {
+        const int c0 = gr.cnt[0], h = (c0 + 1) / 2;
+        const int r = h > gr.cnt[1] ? h : gr.cnt[1];
+        if (r < gr.rounds) {
+          gr.cls |= GRP_SPLIT0;
+          gr.cnt[0] = (uint16_t)h;
+          gr.cnt[3] = (uint16_t)(c0 - h);
+          gr.rounds = (uint16_t)r;
+        }
+      }
+      e_total = (int)align_up(e_total + group_width(gr.n) * gr.rounds, 8);
+    };
     for (int k = 0; k < n_emit; ++k) {
       const typename KT::G key = s.gkey[k];
       const int pos = KT::gpos(key);
@@ -680,7 +695,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       const bool join = ng > 0 && lv == cur_lv && cls == cur_cls && cls == 0 && s.grp[ng - 1].n < 4 &&
                         TNEAT_JOIN_DEN * cnt >= TNEAT_JOIN_NUM * cur_rounds;
       if (!join) {
-        if (ng > 0) e_total = (int)align_up(e_total + group_width(s.grp[ng - 1].n) * s.grp[ng - 1].rounds, 8);
+        if (ng > 0) close(s.grp[ng - 1]);
         GroupRec gr;
         memset(&gr, 0, sizeof(gr));
         // holes (shorter lists in a sum/mean group) read the zero slot
@@ -698,7 +713,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       s.step_row[k] = (uint16_t)row;
       s.grp_of[k] = (uint16_t)(ng - 1);
     }
-    if (ng > 0) e_total = (int)align_up(e_total + group_width(s.grp[ng - 1].n) * s.grp[ng - 1].rounds, 8);
+    if (ng > 0) close(s.grp[ng - 1]);
     s.ready[0] = (uint32_t)ng;  // Kahn is done: ready/indeg serve as scalar mailboxes
     s.indeg[0] = e_total;
   }
@@ -838,9 +853,19 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     st.resp = (T)nr[2];
     steps[k] = st;
     // column j of the group's edge block; holes (and the spare column of a
-    // 3-group) are (zero slot, 0.0) entries
-    const int ncol = (gr.n == 3 && j == 2) ? 2 : 1;
-    for (int col = j; col < j + ncol; ++col) {
+    // 3-group) are (zero slot, 0.0) entries; GRP_SPLIT0: step 0's list goes
+    // to columns 0 (first cnt[0] edges) and 3 (the rest)
+    const bool split0 = (gr.cls & GRP_SPLIT0) != 0;
+    int cols[2] = {j, 3}, first[2] = {0, 0}, nedge[2] = {cnt, 0};
+    int ncol = (gr.n == 3 && j == 2 && !split0) ? 2 : 1;
+    if (split0 && j == 0) {
+      ncol = 2;
+      first[1] = gr.cnt[0];
+      nedge[0] = gr.cnt[0];
+      nedge[1] = cnt - gr.cnt[0];
+    }
+    for (int ci = 0; ci < ncol; ++ci) {
+      const int col = cols[ci];
       // rounds in batches of 4: the weight loads of a batch are in flight together
       for (int rr0 = 0; rr0 < gr.rounds; rr0 += 4) {
         uint32_t src[4];
@@ -850,8 +875,8 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
           const int rr = rr0 + u;
           src[u] = zero_slot;
           w[u] = 0.0;
-          if (col == j && rr < cnt) {
-            const typename KT::E kk = s.ekey[e0 + rr];
+          if (rr < nedge[ci]) {
+            const typename KT::E kk = s.ekey[e0 + first[ci] + rr];
             src[u] = s.slot_of[KT::src(kk)];
             w[u] = gc[KT::row(kk) * 4 + 3];
           }
