@@ -272,3 +272,39 @@ def test_large_host_uploads_staged(tn):
     np.testing.assert_array_equal(sub._cache["slots"], a._cache["slots"][5:17])
     x = torch.randn(12, 300, 32, device="cuda")
     assert torch.equal(tn.forward_device(sub, x), tn.forward_device(b.select(slice(5, 17)), x))
+
+
+def _split0_groups(st) -> int:
+    """Number of GRP_SPLIT0 sum groups in the programs (GroupRec.cls bit 4)."""
+    from paper_2404_01817_b200 import _native  # noqa: F401
+    prog = st.program.cpu().numpy()
+    hdr = prog[:, :32].view(np.int32)
+    off = 32 + ((2 * st.num_outputs + 15) // 16) * 16
+    total = 0
+    for p in range(prog.shape[0]):
+        g = prog[p, off:off + 16 * hdr[p, 7]].reshape(-1, 16)
+        total += int(((g[:, 1] & 4) != 0).sum())
+    return total
+
+
+@pytest.mark.parametrize("precision,tol", [("f64", 1e-9), ("f32", 1e-5)])
+def test_split_groups_every_kernel(tn, precision, tol):
+    """Groups of 3 whose longest list spills into the spare column
+    (GRP_SPLIT0) evaluate correctly in the tile kernel (B >= 192) and the warp
+    kernel (variant 8; the fused-fitness and cart-pole passes share its
+    indexing), in both precisions."""
+    import torch
+    from oracle import arrayneat_oracle as orc
+    nodes, conns = orc.synthetic_population(24, 128, 512, 16, 4, seed=91, variant="M", min_conns=200,
+                                            max_conns_drawn=400)
+    st, cyc = tn.transform_arrays(nodes, conns, 16, 4, precision=precision)
+    assert cyc.size == 0
+    assert _split0_groups(st) > 0
+    dt = np.float64 if precision == "f64" else np.float32
+    x = np.random.default_rng(92).standard_normal((24, 256, 16)).astype(dt)
+    refs = [orc.forward_genome(nodes[p], orc.transform_genome(nodes[p], conns[p], 16, 4), x[p].astype(np.float64))
+            for p in range(24)]
+    for variant in (0, 8):
+        out = tn.forward_device(st, torch.from_numpy(x).cuda(), variant=variant).cpu().numpy()
+        for p in range(24):
+            assert _rel_err(out[p], refs[p]) <= tol, (variant, p)
