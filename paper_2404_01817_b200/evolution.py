@@ -531,6 +531,53 @@ def slot_tables(species: list, fitness, config: NeatConfig):
     return pool, off, size, elite
 
 
+def _slot_tables_device(species: list, fitness, config: NeatConfig) -> tuple:
+    """``slot_tables`` built on the device for large populations: the same
+    parent ranking (three stable device sorts), then the pool, per-slot pool
+    offset/size and elite source by gathers -- no read-back of the ranked heads
+    and no table upload.  Returns int32 device tensors (pool, off, size, elite)."""
+    fit = np.asarray(fitness.cpu().numpy() if isinstance(fitness, torch.Tensor) else fitness)
+    total = config.pop_size
+    ordered = sorted(species, key=lambda s: s.species_key)
+    members = [np.asarray(sp.member_indices) for sp in ordered]
+    sizes = np.array([m.size for m in members], dtype=np.int64)
+    spawn = np.array([sp.spawn_count for sp in ordered], dtype=np.int64)
+    n_surv = np.array([max(1, math.ceil(config.survival_threshold * n)) for n in sizes], dtype=np.int64)
+    n_el = np.minimum(np.minimum(config.genome_elitism, spawn), sizes)
+    if int(spawn.sum()) != total:
+        raise ExtinctionError(f"spawn counts sum to {int(spawn.sum())}, expected {total}")
+    dev = device()
+    rowid = np.full(fit.size, len(ordered), dtype=np.int64)  # genomes of dropped species sort last
+    for k, m in enumerate(members):
+        rowid[m] = k
+    f = torch.from_numpy(np.ascontiguousarray(fit)).to(dev)
+    nan = torch.isnan(f)
+    key = torch.where(nan, torch.zeros_like(f), -f) + 0.0  # -0.0 -> +0.0, ties as in numpy
+    idx = torch.argsort(key, stable=True)
+    idx = idx[torch.argsort(nan[idx].to(torch.int8), stable=True)]
+    rid = torch.from_numpy(rowid).to(dev)
+    order = idx[torch.argsort(rid[idx], stable=True)]  # species rank, fitness desc, index asc
+    starts = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    pooled = np.concatenate([[0], np.cumsum(n_surv)[:-1]]).astype(np.int64)
+    small = torch.from_numpy(np.stack([starts, pooled, n_surv, n_el, spawn])).to(dev)
+    st_d, pooled_d, surv_d, el_d, spawn_d = small
+    ks = torch.arange(len(ordered), device=dev)
+    # pool: the first n_surv members of every species, in species order
+    pseg = torch.repeat_interleave(ks, surv_d)
+    pool = order[st_d[pseg] + torch.arange(pseg.numel(), device=dev) - pooled_d[pseg]]
+    # per slot: species segment, position inside it, elite or pool draw
+    seg = torch.repeat_interleave(ks, spawn_d)
+    slot0 = torch.cumsum(spawn_d, 0) - spawn_d
+    pos = torch.arange(total, device=dev) - slot0[seg]
+    is_el = pos < el_d[seg]
+    elite = torch.where(is_el, order[st_d[seg] + torch.where(is_el, pos, 0)], -1)
+    off = torch.where(is_el, 0, pooled_d[seg])
+    size = torch.where(is_el, 1, surv_d[seg])
+    if pool.numel() == 0:
+        pool = torch.zeros(1, dtype=torch.int64, device=dev)
+    return tuple(t.to(torch.int32) for t in (pool, off, size, elite))
+
+
 def reproduce(pop: PopulationTensors, species: list, fitness, config: NeatConfig, rng,
               allocator: NodeKeyAllocator, threads: int = 1, sequential: bool = False) -> PopulationTensors:
     """Next generation (evolution.py:646-715): slot tables here, then one
@@ -538,18 +585,22 @@ def reproduce(pop: PopulationTensors, species: list, fitness, config: NeatConfig
     (generation, STAGE_REPRODUCE, s) and owns node key base + s."""
     total = config.pop_size
     base_key = allocator.reserve(total)
-    pool, off, size, elite = slot_tables(species, fitness, config)
     nd, cd = _dev64(pop.nodes), _dev64(pop.conns)
     dev = nd.device
     n, c = int(nd.shape[1]), int(cd.shape[1])
     on = torch.empty((total, n, 5), dtype=torch.float64, device=dev)
     oc = torch.empty((total, c, 4), dtype=torch.float64, device=dev)
-    # one host->device copy for the four slot tables; the device views stay
-    # referenced until the launch is enqueued
-    tabs = torch.from_numpy(np.concatenate([pool, off, size, elite]).astype(np.int32)).to(dev)
-    npool = pool.size
-    pool_d, off_d = tabs[:npool], tabs[npool:npool + total]
-    size_d, elite_d = tabs[npool + total:npool + 2 * total], tabs[npool + 2 * total:]
+    count = fitness.numel() if isinstance(fitness, torch.Tensor) else np.asarray(fitness).size
+    if count > SMALL_SLOT_TABLES:
+        pool_d, off_d, size_d, elite_d = _slot_tables_device(species, fitness, config)
+    else:
+        pool, off, size, elite = slot_tables(species, fitness, config)
+        # one host->device copy for the four slot tables; the device views stay
+        # referenced until the launch is enqueued
+        tabs = torch.from_numpy(np.concatenate([pool, off, size, elite]).astype(np.int32)).to(dev)
+        npool = pool.size
+        pool_d, off_d = tabs[:npool], tabs[npool:npool + total]
+        size_d, elite_d = tabs[npool + total:npool + 2 * total], tabs[npool + 2 * total:]
     stage_key = int(np.asarray(rng.child(STAGE_REPRODUCE)._keys).reshape(-1)[0])
     params = mutate_params(config, n, c)
     _native.call("an_reproduce", ptr(nd), ptr(cd), ptr(on), ptr(oc), total, 0, ptr(pool_d), ptr(off_d),

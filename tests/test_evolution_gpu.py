@@ -222,3 +222,7 @@ def test_slot_tables_device_ranking_equals_host(tn, monkeypatch):
     dev = slot_tables(species, fit, cfg)
     for a, b in zip(host, dev):
         assert np.array_equal(a, b)
+    # the tables built entirely on the device (reproduce's large-population path)
+    built = tn.evolution._slot_tables_device(species, fit, cfg)
+    for a, b in zip(host, built):
+        assert np.array_equal(a, b.cpu().numpy())
