@@ -7,6 +7,8 @@ libtneat.so.  Inputs may be numpy arrays (the reference API) or torch tensors
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
@@ -26,11 +28,17 @@ def stream_handle(stream: torch.cuda.Stream | None = None) -> int:
 
 _STAGE_BYTES = 32 << 20
 _stage = {"bufs": None, "events": [None, None]}
+_stage_lock = threading.Lock()  # the staging buffers are shared by every caller thread
 
 
 def _upload_staged(t: torch.Tensor, dev: torch.device) -> torch.Tensor:
     """Large pageable host tensor -> device through two pinned 32 MB staging
     buffers: the DMA of chunk k overlaps the host copy of chunk k+1."""
+    with _stage_lock:
+        return _upload_staged_locked(t, dev)
+
+
+def _upload_staged_locked(t: torch.Tensor, dev: torch.device) -> torch.Tensor:
     if _stage["bufs"] is None:
         _stage["bufs"] = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
     src = t.reshape(-1).view(torch.uint8)
@@ -78,8 +86,13 @@ class _PinnedRing:
         self.bufs = [None] * n
         self.events = [None] * n
         self.k = 0
+        self.lock = threading.Lock()
 
-    def upload(self, arr: np.ndarray, dev: torch.device) -> torch.Tensor:
+    def upload(self, arr: np.ndarray, dev: torch.device):
+        with self.lock:
+            return self._upload(arr, dev)
+
+    def _upload(self, arr: np.ndarray, dev: torch.device):
         src = torch.from_numpy(np.ascontiguousarray(arr))
         nbytes = src.numel() * src.element_size()
         slot = self.k
