@@ -28,11 +28,17 @@ namespace tneat {
 
 constexpr int HN_K = 64;           // substrate inputs
 constexpr int HN_N1 = 64;          // substrate outputs per genome
-constexpr int HN_G = 4;            // genomes per CTA
+#ifndef TNEAT_HN_G
+#define TNEAT_HN_G 4
+#endif
+constexpr int HN_G = TNEAT_HN_G;   // genomes per CTA (2 = two CTAs per SM: 1.41 vs 1.17 ms, slower)
 constexpr int HN_N = HN_N1 * HN_G; // MMA N
 constexpr int HN_M = 128;          // rows per tile (MMA M)
 constexpr int HN_THREADS = 512;        // 16 warps: warp w reads TMEM lanes 32*(w%4).. of
-constexpr int HN_SETS = HN_THREADS / 128; // genomes (w/4)*HN_G/HN_SETS .. in the epilogue
+constexpr int HN_SETS = HN_THREADS / 128; // column sets: warp w reads columns (w/4)*HN_CW.. in the epilogue
+constexpr int HN_CW = HN_N / HN_SETS;     // columns per warp (one genome: HN_CW <= HN_N1)
+constexpr int HN_TMEM_COLS = 2 * HN_N;    // two accumulator stages
+static_assert(HN_CW <= HN_N1 && HN_N1 % HN_CW == 0 && HN_CW % 32 == 0, "epilogue mapping");
 
 // K-major, no-swizzle operands laid out as K-chunk slabs: element (row, k) at
 // (k / 4) * LBO + row * 16 + (k % 4) * 4, i.e. core matrices 8 rows x 16 B with
@@ -67,7 +73,7 @@ __device__ __forceinline__ void tma_a_tile(float* a, const void* tx, int r0, uin
   for (int kc = 0; kc < HN_K / 4; ++kc) tma_load_2d(base + kc * HN_LBO_A, tx, kc * 4, r0, bar);
 }
 
-__global__ void __launch_bounds__(HN_THREADS, 1)
+__global__ void __launch_bounds__(HN_THREADS, 512 / HN_TMEM_COLS)
 substrate_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, int64_t P,
                  const float* __restrict__ target, int S, double* __restrict__ fitness) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -77,8 +83,8 @@ substrate_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_consta
   const int ng = (int)(P - g0 < HN_G ? P - g0 : HN_G);
 
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(&sm.tmem_base))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)), "n"(HN_TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -104,31 +110,27 @@ substrate_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_consta
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = sm.tmem_base;
   const int tiles = S / HN_M;
-  float acc_err[HN_G] = {0.f, 0.f, 0.f, 0.f};
+  float acc_err = 0.f;  // this warp's genome
   uint32_t phase[2] = {0u, 0u};
 
   auto epilogue = [&](int tile, int stage) {
     // tile row = TMEM lane = 32 * (warp % 4) + lane; warp / 4 picks the genome set
     const int row = (warp & 3) * 32 + lane;
     const float tv = target[(int64_t)tile * HN_M + row];
-    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(stage * HN_N);
-    constexpr int GS = HN_G / HN_SETS;
-#pragma unroll
-    for (int gg = 0; gg < GS; ++gg) {
-      const int g = (warp >> 2) * GS + gg;
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(stage * HN_N) +
+                           (uint32_t)((warp >> 2) * HN_CW);
 #pragma unroll 1
-      for (int q = 0; q < HN_N1 / 16; q += 2) {  // two 16-column loads per wait
-        uint32_t r[16], r2[16];
-        TMEM_LD16(taddr + g * HN_N1 + q * 16, r);
-        TMEM_LD16(taddr + g * HN_N1 + (q + 1) * 16, r2);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    for (int q = 0; q < HN_CW / 16; q += 2) {  // two 16-column loads per wait
+      uint32_t r[16], r2[16];
+      TMEM_LD16(taddr + q * 16, r);
+      TMEM_LD16(taddr + (q + 1) * 16, r2);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float d = tanh_approx(__uint_as_float(r[i])) - tv;
-          const float d2 = tanh_approx(__uint_as_float(r2[i])) - tv;
-          acc_err[gg] = fmaf(d, d, acc_err[gg]);
-          acc_err[gg] = fmaf(d2, d2, acc_err[gg]);
-        }
+      for (int i = 0; i < 16; ++i) {
+        const float d = tanh_approx(__uint_as_float(r[i])) - tv;
+        const float d2 = tanh_approx(__uint_as_float(r2[i])) - tv;
+        acc_err = fmaf(d, d, acc_err);
+        acc_err = fmaf(d2, d2, acc_err);
       }
     }
   };
@@ -167,18 +169,14 @@ substrate_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_consta
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     epilogue(last, stage);
   }
-  // reduce squared errors over the CTA's 128 rows (each warp holds GS genomes)
+  // reduce squared errors over the CTA's 128 rows (each warp holds one genome's columns)
   {
-    constexpr int GS = HN_G / HN_SETS;
     if (lane < HN_G) sm.part[warp][lane] = 0.f;
     __syncwarp();
+    float v = acc_err;
 #pragma unroll
-    for (int gg = 0; gg < GS; ++gg) {
-      float v = acc_err[gg];
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-      if (lane == 0) sm.part[warp][(warp >> 2) * GS + gg] = v;
-    }
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if (lane == 0) sm.part[warp][(warp >> 2) * HN_CW / HN_N1] = v;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -189,7 +187,7 @@ substrate_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_consta
   }
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(HN_TMEM_COLS) : "memory");
   }
 }
 
