@@ -45,7 +45,7 @@ CONFIG = {
 def _parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -62,7 +62,7 @@ def _parse():
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
-    """SM clock and throttle reasons sampled every 50 ms during the timed
+    """SM clock and throttle reasons sampled every 20 ms during the timed
     region, in-process through NVML (no nvidia-smi child competing for the
     driver); falls back to `nvidia-smi -lms` when NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -90,7 +90,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             return
@@ -110,7 +110,7 @@ class ClockSampler:
                 break
             self.samples.append((time.perf_counter(), [str(sm), str(mx)] +
                                  ["Active" if r & b else "Not Active" for b in bits]))
-            self.stop_evt.wait(0.05)
+            self.stop_evt.wait(0.02)
 
     def _read(self):
         for line in self.proc.stdout:
