@@ -120,9 +120,9 @@ __device__ __forceinline__ void load_words(Words& d, const uint32_t* off_s, cons
 
 // two rounds of a sum group: 2*GW value loads (byte offsets into the thread's
 // value column), then one FFMA2 (or FFMA for S = 1) per edge and sample pair
-template <int S, int G, int GW>
-__device__ __forceinline__ void sum_rounds(float2 (&acc)[G][(S + 1) / 2], const uint32_t (&off)[2 * GW],
-                                           const float (&w)[2 * GW], const char* vb) {
+template <int S, int G, int GW, typename OffA, typename WA>
+__device__ __forceinline__ void sum_rounds(float2 (&acc)[G][(S + 1) / 2], const OffA& off, const WA& w,
+                                           const char* vb) {
   using PackT = Pack<float, S>;
   PackT v[2 * GW];
 #pragma unroll
@@ -149,9 +149,9 @@ __device__ __forceinline__ void sum_rounds(float2 (&acc)[G][(S + 1) / 2], const 
 }
 
 // one round (the first GW entries of a two-round buffer)
-template <int S, int G, int GW>
-__device__ __forceinline__ void sum_round1(float2 (&acc)[G][(S + 1) / 2], const uint32_t (&off)[2 * GW],
-                                           const float (&w)[2 * GW], const char* vb) {
+template <int S, int G, int GW, typename OffA, typename WA>
+__device__ __forceinline__ void sum_round1(float2 (&acc)[G][(S + 1) / 2], const OffA& off, const WA& w,
+                                           const char* vb) {
   using PackT = Pack<float, S>;
   PackT v[GW];
 #pragma unroll
@@ -181,8 +181,8 @@ __device__ __forceinline__ void sum_round1(float2 (&acc)[G][(S + 1) / 2], const 
 template <int S, int G, int RB, bool TANH, bool MERGE = false>
 __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t* __restrict__ off_s,
                                               const float* __restrict__ w_s,
-                                              const StepT<float>* __restrict__ st, char* vb,
-                                              const Words* pre = nullptr) {
+                                              const StepT<float>* __restrict__ st, char* vb, Words& wd,
+                                              int next_e) {
   constexpr int GW = G == 3 ? 4 : G;
   constexpr int NS = MERGE ? G - 1 : G;  // steps
   constexpr int SP = (S + 1) / 2;  // sample pairs: Blackwell packed fp32 (FFMA2 / FADD2)
@@ -210,32 +210,46 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
   const int rounds = gr.rounds;  // holes read the zero slot with weight 0
   uint32_t oa[2 * GW], ob[2 * GW];
   float wa[2 * GW], wb[2 * GW];
-  if (pre) {
-#pragma unroll
-    for (int q = 0; q < 2 * GW; ++q) { oa[q] = pre->o[q]; wa[q] = pre->w[q]; }
-  } else if (rounds > 0) {
-    load_u32<2 * GW>(op, oa);
-    load_f32<2 * GW>(wp, wa);
+  // rounds 0-1 come from `wd` (prefetched by the previous group); after the
+  // last round `wd` takes the next group's first words in place (no copies)
+  bool more = false;
+  if (rounds < 2) {
+    if (rounds == 1) sum_round1<S, G, GW>(acc, wd.o, wd.w, vb);
+  } else {
+    load_u32<2 * GW>(op + 2 * GW, ob);
+    load_f32<2 * GW>(wp + 2 * GW, wb);
+    sum_rounds<S, G, GW>(acc, wd.o, wd.w, vb);
+    if (rounds < 4) {
+      if (rounds == 3) sum_round1<S, G, GW>(acc, ob, wb, vb);
+    } else {
+      load_u32<2 * GW>(op + 4 * GW, oa);
+      load_f32<2 * GW>(wp + 4 * GW, wa);
+      sum_rounds<S, G, GW>(acc, ob, wb, vb);
+      more = true;
+    }
   }
-  // round pairs from alternating buffers; an odd last round from the first
-  // half of the buffer that holds it
+  // round pairs from alternating buffers (loads one pair ahead); an odd last
+  // round from the first half of the buffer that holds it
+  if (more) {
 #pragma unroll 1
-  for (int r = 0;; r += 4) {
-    if (r + 2 > rounds) {
-      if (r < rounds) sum_round1<S, G, GW>(acc, oa, wa, vb);
-      break;
+    for (int r = 4;; r += 4) {
+      if (r + 2 > rounds) {
+        if (r < rounds) sum_round1<S, G, GW>(acc, oa, wa, vb);
+        break;
+      }
+      load_u32<2 * GW>(op + (r + 2) * GW, ob);
+      load_f32<2 * GW>(wp + (r + 2) * GW, wb);
+      sum_rounds<S, G, GW>(acc, oa, wa, vb);
+      if (r + 4 > rounds) {
+        if (r + 2 < rounds) sum_round1<S, G, GW>(acc, ob, wb, vb);
+        break;
+      }
+      load_u32<2 * GW>(op + (r + 4) * GW, oa);
+      load_f32<2 * GW>(wp + (r + 4) * GW, wa);
+      sum_rounds<S, G, GW>(acc, ob, wb, vb);
     }
-    load_u32<2 * GW>(op + (r + 2) * GW, ob);
-    load_f32<2 * GW>(wp + (r + 2) * GW, wb);
-    sum_rounds<S, G, GW>(acc, oa, wa, vb);
-    if (r + 4 > rounds) {
-      if (r + 2 < rounds) sum_round1<S, G, GW>(acc, ob, wb, vb);
-      break;
-    }
-    load_u32<2 * GW>(op + (r + 4) * GW, oa);
-    load_f32<2 * GW>(wp + (r + 4) * GW, wa);
-    sum_rounds<S, G, GW>(acc, ob, wb, vb);
   }
+  load_words(wd, off_s, w_s, next_e);  // in flight during the epilogue
   if constexpr (MERGE) {
 #pragma unroll
     for (int p = 0; p < SP; ++p) acc[0][p] = __fadd2_rn(acc[0][p], acc[G - 1][p]);
@@ -378,29 +392,29 @@ __device__ __forceinline__ void run_generic_step(const GroupRec& gr, const uint3
 
 template <typename T, int S, int RB>
 __device__ __forceinline__ void run_group(const GroupRec& gr, const uint32_t* src_s, const float* w_s,
-                                          const EdgeD* ed_s, const StepT<T>* st, char* vb,
-                                          const Words* pre = nullptr) {
+                                          const EdgeD* ed_s, const StepT<T>* st, char* vb, Words& wd,
+                                          int next_e) {
   if (!(gr.cls & GRP_GENERIC)) {
     if constexpr (sizeof(T) == 4) {
       if (gr.cls & GRP_TANH_SUM) {
         switch (gr.n) {
-          case 1: run_sum_group<S, 1, RB, true>(gr, src_s, w_s, st, vb, pre); break;
-          case 2: run_sum_group<S, 2, RB, true>(gr, src_s, w_s, st, vb, pre); break;
+          case 1: run_sum_group<S, 1, RB, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
+          case 2: run_sum_group<S, 2, RB, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
           case 3:
-            if (gr.cls & GRP_SPLIT0) run_sum_group<S, 4, RB, true, true>(gr, src_s, w_s, st, vb, pre);
-            else run_sum_group<S, 3, RB, true>(gr, src_s, w_s, st, vb, pre);
+            if (gr.cls & GRP_SPLIT0) run_sum_group<S, 4, RB, true, true>(gr, src_s, w_s, st, vb, wd, next_e);
+            else run_sum_group<S, 3, RB, true>(gr, src_s, w_s, st, vb, wd, next_e);
             break;
-          default: run_sum_group<S, 4, RB, true>(gr, src_s, w_s, st, vb, pre); break;
+          default: run_sum_group<S, 4, RB, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
         }
       } else {
         switch (gr.n) {
-          case 1: run_sum_group<S, 1, RB, false>(gr, src_s, w_s, st, vb, pre); break;
-          case 2: run_sum_group<S, 2, RB, false>(gr, src_s, w_s, st, vb, pre); break;
+          case 1: run_sum_group<S, 1, RB, false>(gr, src_s, w_s, st, vb, wd, next_e); break;
+          case 2: run_sum_group<S, 2, RB, false>(gr, src_s, w_s, st, vb, wd, next_e); break;
           case 3:
-            if (gr.cls & GRP_SPLIT0) run_sum_group<S, 4, RB, false, true>(gr, src_s, w_s, st, vb, pre);
-            else run_sum_group<S, 3, RB, false>(gr, src_s, w_s, st, vb, pre);
+            if (gr.cls & GRP_SPLIT0) run_sum_group<S, 4, RB, false, true>(gr, src_s, w_s, st, vb, wd, next_e);
+            else run_sum_group<S, 3, RB, false>(gr, src_s, w_s, st, vb, wd, next_e);
             break;
-          default: run_sum_group<S, 4, RB, false>(gr, src_s, w_s, st, vb, pre); break;
+          default: run_sum_group<S, 4, RB, false>(gr, src_s, w_s, st, vb, wd, next_e); break;
         }
       }
     } else {
@@ -412,6 +426,7 @@ __device__ __forceinline__ void run_group(const GroupRec& gr, const uint32_t* sr
       }
     }
   } else {
+    if constexpr (sizeof(T) == 4) load_words(wd, src_s, w_s, next_e);
     run_generic_step<T, S, RB>(gr, src_s, w_s, ed_s, st[0], vb);
   }
 }
@@ -586,17 +601,16 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
     // (two records ahead), and -- fp32 -- the next group's first program words
     uint4 raw_next = reinterpret_cast<const uint4*>(gr_s)[0];
     uint4 raw_next2 = reinterpret_cast<const uint4*>(gr_s)[1];
-    Words cur, nxt;
+    Words wd;  // the current group's first words; refilled in place with the next group's
     if constexpr (sizeof(T) == 4) {
-      if (n_groups > 0) load_words(cur, src_s, w_s, (int)(raw_next.y & 0xFFFF));
+      if (n_groups > 0) load_words(wd, src_s, w_s, (int)(raw_next.y & 0xFFFF));
     }
 #pragma unroll 1
     for (int g = 0; g < n_groups; ++g) {
       const uint4 raw = raw_next;
       raw_next = raw_next2;
       raw_next2 = reinterpret_cast<const uint4*>(gr_s)[g + 2];
-      if constexpr (sizeof(T) == 4)
-        load_words(nxt, src_s, w_s, g + 1 < n_groups ? (int)(raw_next.y & 0xFFFF) : 0);
+      const int next_e = g + 1 < n_groups ? (int)(raw_next.y & 0xFFFF) : 0;
       GroupRec gr;
       gr.n = (uint8_t)(raw.x & 0xFF);
       gr.cls = (uint8_t)((raw.x >> 8) & 0xFF);
@@ -607,8 +621,7 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
       gr.cnt[1] = (uint16_t)(raw.z >> 16);
       gr.cnt[2] = (uint16_t)(raw.w & 0xFFFF);
       gr.cnt[3] = (uint16_t)(raw.w >> 16);
-      run_group<T, S, RB>(gr, src_s, w_s, ed_s, st_s + gr.step_begin, vb, sizeof(T) == 4 ? &cur : nullptr);
-      if constexpr (sizeof(T) == 4) cur = nxt;
+      run_group<T, S, RB>(gr, src_s, w_s, ed_s, st_s + gr.step_begin, vb, wd, next_e);
     }
 
     // outputs (P, B, O): one S-wide load per output slot, 16-byte stores per input
