@@ -255,6 +255,7 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
     for (int p = 0; p < SP; ++p) acc[0][p] = __fadd2_rn(acc[0][p], acc[G - 1][p]);
   }
   if constexpr (TANH) {
+    const uint32_t vbs = (uint32_t)__cvta_generic_to_shared(vb);
     // tanh(b + r*a) = 2 / (1 + 2^(k (b + r*a))) - 1, k = -2 log2(e): one FFMA into
     // EX2 (k folded into b and r once per step), FADD, RCP, FFMA -- |err| <~ 2e-7
 #pragma unroll
@@ -278,7 +279,14 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
           y.v[2 * p + 1] = yy.y;
         }
       }
-      if (slot_j[j] != NO_SLOT) *reinterpret_cast<PackT*>(vb + slot_j[j] * RB) = y;
+      if (slot_j[j] != NO_SLOT) {
+        if constexpr (S == 2) {  // explicit shared store: the window base is computed once per group
+          asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(vbs + slot_j[j] * RB), "f"(y.v[0]), "f"(y.v[1])
+                       : "memory");
+        } else {
+          *reinterpret_cast<PackT*>(vb + slot_j[j] * RB) = y;
+        }
+      }
     }
   } else {
 #pragma unroll
