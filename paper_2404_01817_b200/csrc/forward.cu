@@ -560,11 +560,15 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
         // store their components in the order 2,0,3,1 (lower: 0,2,1,3), so the
         // 8 rows of each store have distinct even residues mod 16 and the
         // store is conflict-free.
+        // c & 7 == tid & 7 (NT is a multiple of 8): the lane's swizzle is fixed
+        // (hoisted out of the loop; batching several loads per thread before
+        // the stores measured slower)
+        const bool hi = (tid & 4) != 0;
+        const int o2 = hi ? 0 : 2 * (RB / 4), o0 = hi ? 2 * (RB / 4) : 0;
+        float* const cbase = vf + ((tid & 7) << 2) * (RB / 4);
         for (int c = tid; c < n4; c += NT) {
           const float4 x = __ldg(src + c);
-          const bool hi = (c & 4) != 0;
-          float* base = vf + (c >> 3) + ((c & 7) << 2) * (RB / 4);
-          const int o2 = hi ? 0 : 2 * (RB / 4), o0 = hi ? 2 * (RB / 4) : 0;
+          float* base = cbase + (c >> 3);
           base[o0] = hi ? x.z : x.x;
           base[o2] = hi ? x.x : x.z;
           base[o0 + (RB / 4)] = hi ? x.w : x.y;
