@@ -279,13 +279,12 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
           y.v[2 * p + 1] = yy.y;
         }
       }
-      if (slot_j[j] != NO_SLOT) {
-        if constexpr (S == 2) {  // explicit shared store: the window base is computed once per group
-          asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(vbs + slot_j[j] * RB), "f"(y.v[0]), "f"(y.v[1])
-                       : "memory");
-        } else {
-          *reinterpret_cast<PackT*>(vb + slot_j[j] * RB) = y;
-        }
+      // every step has a slot (the transform gives unread steps a scratch slot)
+      if constexpr (S == 2) {  // explicit shared store: the window base is computed once per group
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(vbs + slot_j[j] * RB), "f"(y.v[0]), "f"(y.v[1])
+                     : "memory");
+      } else {
+        *reinterpret_cast<PackT*>(vb + slot_j[j] * RB) = y;
       }
     }
   } else {

@@ -778,6 +778,16 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       __syncwarp();
     }
   }
+  // steps whose value nobody reads (unpruned programs) write a scratch slot:
+  // every step has a slot, so kernels store step results unconditionally
+  bool orphan = false;
+  for (int k = lane; k < n_emit; k += 32) {
+    const int row = s.step_row[k];
+    orphan |= !(s.used[row] || (s.flags[row] & F_OUTPUT));
+  }
+  orphan = __any_sync(0xffffffffu, orphan);
+  const uint16_t scratch_slot = orphan ? (uint16_t)n_slots : NO_SLOT;
+  if (orphan) n_slots += 1;
   const uint32_t zero_slot = (uint32_t)n_slots;
   n_slots += 1;
   // ---- write groups, steps and interleaved edge lists --------------------------
@@ -796,7 +806,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       StepT<T> st;
       memset(&st, 0, sizeof(st));
       const int e0 = s.in_start[row], cnt = s.in_start[row + 1] - e0;
-      st.slot = (s.used[row] || (s.flags[row] & F_OUTPUT)) ? s.slot_of[row] : NO_SLOT;
+      st.slot = (s.used[row] || (s.flags[row] & F_OUTPUT)) ? s.slot_of[row] : scratch_slot;
       st.act = (uint8_t)((av >= 0.0 && av < ACT_COUNT) ? (int)av : 0);
       st.agg = (uint8_t)((gv >= 0.0 && gv < AGG_COUNT) ? (int)gv : 0);
       st.count = (uint16_t)cnt;
@@ -845,7 +855,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     StepT<T> st;
     memset(&st, 0, sizeof(st));
     const int e0 = s.in_start[row], cnt = s.in_start[row + 1] - e0;
-    st.slot = (s.used[row] || (s.flags[row] & F_OUTPUT)) ? s.slot_of[row] : NO_SLOT;
+    st.slot = (s.used[row] || (s.flags[row] & F_OUTPUT)) ? s.slot_of[row] : scratch_slot;
     st.act = (uint8_t)((av >= 0.0 && av < ACT_COUNT) ? (int)av : 0);
     st.agg = (uint8_t)((gv >= 0.0 && gv < AGG_COUNT) ? (int)gv : 0);
     st.count = (uint16_t)cnt;
