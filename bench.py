@@ -199,7 +199,7 @@ def run_reference(args, rank: int) -> None:
     threads = min(os.cpu_count() or 1, 32)
     nodes, conns = synthetic_population(max(64, 4 * threads), MAXN, MAXC, NIN, NOUT, seed=20261018)
     x = np.random.default_rng(20261019).standard_normal((nodes.shape[0], BATCH, NIN), dtype=np.float32)
-    per_step = max(2.0, min(10.0, 90.0 / max(1, args.steps + args.warmup)))
+    per_step = max(0.5, min(10.0, 60.0 / max(1, args.steps + args.warmup)))  # whole run ~1 min
     for _ in range(args.warmup):
         cpu_forward_rate(nodes, conns, x, per_step / 4, threads)
     rates = [cpu_forward_rate(nodes, conns, x, per_step, threads) for _ in range(args.steps)]
