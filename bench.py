@@ -45,7 +45,7 @@ CONFIG = {
 def _parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -153,6 +153,9 @@ def _load_reference():
     return None, "port"
 
 
+_CAL: dict = {}
+
+
 def cpu_forward_rate(nodes, conns, x, seconds: float, threads: int | None = None) -> dict:
     """Time the reference transform+forward on a bounded sample of the same
     workload, genome work items of 4 (bounds the (P,B,N) float64
@@ -175,10 +178,12 @@ def cpu_forward_rate(nodes, conns, x, seconds: float, threads: int | None = None
                 tr = orc.transform_genome(nodes[p], conns[p], NIN, NOUT)
                 orc.forward_genome(nodes[p], tr, x[p].astype(np.float64))
             return None
-    # calibrate on one item, then size the sample to ~`seconds`
-    t = time.perf_counter()
-    work(0)
-    per_item = time.perf_counter() - t
+    # calibrate on one item (once per process), then size the sample to ~`seconds`
+    per_item = _CAL.get(kind)
+    if per_item is None:
+        t = time.perf_counter()
+        work(0)
+        per_item = _CAL[kind] = time.perf_counter() - t
     n_items = max(threads, int(seconds * threads / max(per_item, 1e-3)))
     n_items = min(n_items, nodes.shape[0] // item)
     starts = [(k * item) % (nodes.shape[0] - item + 1) for k in range(n_items)]
