@@ -228,25 +228,30 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
       more = true;
     }
   }
-  // round pairs from alternating buffers (loads one pair ahead); an odd last
-  // round from the first half of the buffer that holds it
+  // round pairs from alternating buffers (loads one pair ahead; `oa` holds
+  // rounds r, r+1 on entry), a single exit so the accumulators keep their
+  // registers across iterations; then the last 0-3 rounds
   if (more) {
+    int r = 4;
 #pragma unroll 1
-    for (int r = 4;; r += 4) {
-      if (r + 2 > rounds) {
-        if (r < rounds) sum_round1<S, G, GW>(acc, oa, wa, vb);
-        break;
-      }
+    for (; r + 4 <= rounds; r += 4) {
       load_u32<2 * GW>(op + (r + 2) * GW, ob);
       load_f32<2 * GW>(wp + (r + 2) * GW, wb);
       sum_rounds<S, G, GW>(acc, oa, wa, vb);
-      if (r + 4 > rounds) {
-        if (r + 2 < rounds) sum_round1<S, G, GW>(acc, ob, wb, vb);
-        break;
-      }
       load_u32<2 * GW>(op + (r + 4) * GW, oa);
       load_f32<2 * GW>(wp + (r + 4) * GW, wa);
       sum_rounds<S, G, GW>(acc, ob, wb, vb);
+    }
+    const int rem = rounds - r;
+    if (rem >= 2) {
+      if (rem == 3) {
+        load_u32<2 * GW>(op + (r + 2) * GW, ob);
+        load_f32<2 * GW>(wp + (r + 2) * GW, wb);
+      }
+      sum_rounds<S, G, GW>(acc, oa, wa, vb);
+      if (rem == 3) sum_round1<S, G, GW>(acc, ob, wb, vb);
+    } else if (rem == 1) {
+      sum_round1<S, G, GW>(acc, oa, wa, vb);
     }
   }
   load_words(wd, off_s, w_s, next_e);  // in flight during the epilogue
