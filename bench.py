@@ -295,6 +295,9 @@ def run_ours(args, rank: int, world: int) -> None:
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    import gc
+    gc.collect()
+    gc.disable()  # no collector pauses between the host's per-step launches
     sampler = ClockSampler(dev.index)
     sampler.start()
     time.sleep(0.2)
@@ -306,7 +309,11 @@ def run_ours(args, rank: int, world: int) -> None:
     s0.record(fw)
     tr.wait_event(s0)
     st = None
+    trace = os.environ.get("TNEAT_BENCH_TRACE")  # diagnostics: per-step host times to stderr
+    host_t = []
     for _ in range(args.steps):
+        if trace:
+            host_t.append(time.perf_counter())
         st = step()
     done = torch.cuda.Event()
     done.record(tr)
@@ -316,6 +323,11 @@ def run_ours(args, rank: int, world: int) -> None:
     if world > 1:
         dist.barrier()
     t_wall1 = time.perf_counter()
+    gc.enable()
+    if trace and host_t:
+        gaps = np.diff(np.array(host_t + [t_wall1])) * 1e3
+        print(f"trace: host ms per step median {np.median(gaps):.2f} max {gaps.max():.2f} "
+              f"at step {int(gaps.argmax())}; total {1e3 * (t_wall1 - host_t[0]):.1f} ms", file=sys.stderr)
     elapsed = s0.elapsed_time(s1) / 1e3
     # forward kernel time for the roofline: the same forward, not overlapped
     pairs = []

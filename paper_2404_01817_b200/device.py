@@ -101,8 +101,15 @@ class _PinnedRing:
             self.events[slot].synchronize()
         buf = self.bufs[slot]
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, pin_memory=True)
-            self.bufs[slot] = buf
+            # pinned allocations are slow (milliseconds): size every slot at once,
+            # with headroom, so steady-state uploads never allocate
+            size = max(2 * nbytes, 1 << 20)
+            for k in range(len(self.bufs)):
+                if self.bufs[k] is None or self.bufs[k].numel() < nbytes:
+                    if self.events[k] is not None:
+                        self.events[k].synchronize()
+                    self.bufs[k] = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+            buf = self.bufs[slot]
         staged = buf[:nbytes].view(src.dtype).view(src.shape)
         staged.copy_(src)
         out = torch.empty(src.shape, dtype=src.dtype, device=dev)
