@@ -260,12 +260,15 @@ def finalize_transform(stacked: StackedNetworks) -> np.ndarray:
     md = stacked._cache.pop("maxdims_dev", None)
     if md is not None:
         # one read-back: launch sizes, per-genome status and value-slot counts
-        slots = stacked.program[:, 8:12].contiguous().view(torch.int32).reshape(-1)
-        host = torch.cat([md, stacked.status_dev, slots]).cpu().numpy()
+        # header words 0-2: steps, edge entries, value slots (common.cuh ProgHeader)
+        dims = stacked.program[:, 0:12].contiguous().view(torch.int32).reshape(-1)
+        host = torch.cat([md, stacked.status_dev, dims]).cpu().numpy()
         p = stacked.size
         stacked.maxdims = tuple(int(v) for v in host[:3])
         stacked._cache["status"] = host[3:3 + p]
-        stacked._cache["slots"] = host[3 + p:]
+        d3 = host[3 + p:].reshape(p, 3)
+        stacked._cache["slots"] = d3[:, 2]
+        stacked._cache["steps_edges"] = d3[:, :2]
     return status_cyclic(stacked.status, stacked.mode)
 
 
@@ -362,13 +365,21 @@ def _bucket_plan(stacked: StackedNetworks, variant: int) -> list:
     else:
         pad = {1: 1, 2: 2, 3: 1, 4: 4, 5: 2, 6: 4}[variant]
         occ = _SMEM_PER_SM // (prog + np.maximum(sorted_slots, stacked.num_inputs) * (tt + pad) * esz + 1024)
+    # per-bucket program extents (steps, edge entries) when the read-back has them:
+    # a launch sizes its shared program area for its own genomes, not the population's
+    # largest (fp32 tile kernel only; the classes above stay conservative)
+    se = stacked._cache.get("steps_edges") if variant != V_SPLIT and not stacked.precision & FMT_F64 else None
     plan = []
     lo = 0
     n = sorted_slots.size
     while lo < n:
         hi = lo + int(np.searchsorted(occ[lo:] != occ[lo], True))  # first index with another class
         hi = n if hi == lo else hi
-        plan.append((ids[lo:hi], (int(sorted_slots[hi - 1]), ms, me)))
+        if se is not None:
+            ext = se[order[lo:hi]].max(axis=0)
+            plan.append((ids[lo:hi], (int(sorted_slots[hi - 1]), int(ext[0]), int(ext[1]))))
+        else:
+            plan.append((ids[lo:hi], (int(sorted_slots[hi - 1]), ms, me)))
         lo = hi
     stacked._cache[key] = plan
     return plan
