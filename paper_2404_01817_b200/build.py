@@ -47,9 +47,25 @@ def _stale(obj: str, src: str) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _flags_changed(extra: list[str]) -> bool:
+    """The objects record the flags they were built with (a stamp file): a
+    build with different TNEAT_NVCC_EXTRA knobs (diagnostic -D switches compute
+    wrong outputs by design) never leaves its objects behind for a plain build."""
+    stamp = os.path.join(BUILD, "flags.stamp")
+    key = " ".join(ARCH + FLAGS + extra + [f"{k}:{' '.join(v)}" for k, v in sorted(PER_FILE.items())])
+    old = open(stamp).read() if os.path.exists(stamp) else None
+    if old != key:
+        with open(stamp, "w") as f:
+            f.write(key)
+        return old is not None or any(f.endswith(".o") for f in os.listdir(BUILD))
+    return False
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     nvcc = _nvcc()
     os.makedirs(BUILD, exist_ok=True)
+    extra = os.environ.get("TNEAT_NVCC_EXTRA", "").split()  # tuning experiments (-D knobs) only
+    force = _flags_changed(extra) or force
     srcs = sources()
     objs = [os.path.join(BUILD, os.path.basename(s)[:-3] + ".o") for s in srcs]
 
@@ -57,7 +73,6 @@ def build(verbose: bool = False, force: bool = False) -> str:
         src, obj = pair
         if not force and not _stale(obj, src):
             return obj, ""
-        extra = os.environ.get("TNEAT_NVCC_EXTRA", "").split()  # tuning experiments (-D knobs) only
         cmd = [nvcc, *ARCH, *FLAGS, *PER_FILE.get(os.path.basename(src), []), *extra, "-I", CSRC, "-c", src,
                "-o", obj]
         if verbose:

@@ -20,6 +20,32 @@ CONN_IN, CONN_OUT, CONN_ENABLED, CONN_WEIGHT = range(4)
 NODE_ATTRS, CONN_ATTRS = 4, 2
 
 
+@dataclass(frozen=True)
+class NodeRow:
+    """A live node gene as a record (genome.py:38-50)."""
+    key: int
+    bias: float
+    response: float
+    aggregation_id: int
+    activation_id: int
+
+    def as_array(self) -> np.ndarray:
+        return np.asarray((self.key, self.bias, self.response, self.aggregation_id, self.activation_id),
+                          dtype=np.float64)
+
+
+@dataclass(frozen=True)
+class ConnRow:
+    """A live connection gene as a record; enabled is 0.0 / 1.0 (genome.py:52-63)."""
+    in_key: int
+    out_key: int
+    enabled: float
+    weight: float
+
+    def as_array(self) -> np.ndarray:
+        return np.asarray((self.in_key, self.out_key, self.enabled, self.weight), dtype=np.float64)
+
+
 @dataclass(frozen=True, eq=False)
 class GenomeTensors:
     """One genome (genome.py:65-79)."""
@@ -106,3 +132,17 @@ def init_genome(config, rng) -> GenomeTensors:
     """Single fresh genome (genome.py:163-166)."""
     nodes, conns = init_arrays(config, rng)
     return GenomeTensors(nodes, conns, config.inputs, config.outputs)
+
+
+def genomes_equal(a: GenomeTensors, b: GenomeTensors) -> bool:
+    """Bit-for-bit equality, NaN padding rows included (genome.py:118-123)."""
+    if (a.num_inputs, a.num_outputs) != (b.num_inputs, b.num_outputs):
+        return False
+    return all(np.array_equal(np.asarray(x), np.asarray(y), equal_nan=True)
+               for x, y in ((a.nodes, b.nodes), (a.conns, b.conns)))
+
+
+def count_live(genome: GenomeTensors) -> tuple[int, int]:
+    """Live (non-padding) node and connection rows (genome.py:279-283)."""
+    live = lambda t: int(np.count_nonzero(~np.all(np.isnan(np.asarray(t)), axis=1)))  # noqa: E731
+    return live(genome.nodes), live(genome.conns)

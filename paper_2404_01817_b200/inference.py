@@ -152,13 +152,14 @@ class StackedNetworks:
         """Row subset (a view on the same device buffers where possible).  The
         host copies of status and slot counts carry over, so planning a subset's
         launches needs no device read-back."""
+        ensure_finalized(self)
         sub = StackedNetworks(self.nodes_dev[idx], self.conns_dev[idx], self.num_inputs,
                               self.num_outputs, self.program[idx],
                               None if self.order_dev is None else self.order_dev[idx],
                               self.conn_rows[idx], self.io_rows[idx], self.status_dev[idx],
                               self.maxdims, self.precision, self.mode)
         if isinstance(idx, slice):
-            for k in ("status", "slots"):
+            for k in ("status", "slots", "steps_edges"):
                 if k in self._cache:
                     sub._cache[k] = self._cache[k][idx]
         return sub
@@ -166,6 +167,8 @@ class StackedNetworks:
     @classmethod
     def from_networks(cls, networks: list) -> "StackedNetworks":
         parts = [t.stacked if isinstance(t, TransformedNetwork) else t for t in networks]
+        for p in parts:  # launch sizes must be known before they are combined
+            ensure_finalized(p)
         first = parts[0]
         md = tuple(max(p.maxdims[k] for p in parts) for k in range(3))
         cat = lambda name: torch.cat([getattr(p, name) for p in parts])  # noqa: E731
@@ -270,6 +273,15 @@ def finalize_transform(stacked: StackedNetworks) -> np.ndarray:
         stacked._cache["slots"] = d3[:, 2]
         stacked._cache["steps_edges"] = d3[:, :2]
     return status_cyclic(stacked.status, stacked.mode)
+
+
+def ensure_finalized(stacked: StackedNetworks) -> None:
+    """Launch sizes come from ``finalize_transform``'s read-back; a transform
+    run with ``sync=False`` is finalized here before anything is launched on it
+    (a launch sized from the (0,0,0) placeholder would under-allocate shared
+    memory)."""
+    if "maxdims_dev" in stacked._cache:
+        finalize_transform(stacked)
 
 
 def status_cyclic(st: np.ndarray, mode: int = 0) -> np.ndarray:
@@ -391,6 +403,7 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
     """Device-resident forward: inputs (P,B,I) (or (B,I) with shared=True) on
     the GPU in the program's dtype -> outputs (P,B,O).  No host syncs after
     the first call on a given StackedNetworks (the bucket plan is cached)."""
+    ensure_finalized(stacked)
     dt = _TORCH_DT[stacked.precision]
     if inputs.dtype != dt or not inputs.is_cuda or not inputs.is_contiguous():
         raise ValueError(f"inputs must be a contiguous CUDA {dt} tensor")
@@ -407,6 +420,10 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
         raise InvalidInput(f"expected input length {stacked.num_inputs}, got {i}")
     if out is None:
         out = torch.empty((pop, b, stacked.num_outputs), dtype=dt, device=inputs.device)
+    elif (not isinstance(out, torch.Tensor) or not out.is_cuda or out.dtype != dt or not out.is_contiguous()
+          or tuple(out.shape) != (pop, b, stacked.num_outputs) or out.device != inputs.device):
+        raise ValueError(f"out must be a contiguous CUDA {dt} tensor of shape (P={pop}, B={b}, "
+                         f"O={stacked.num_outputs}) on {inputs.device}")
     if stacked.precision & FMT_SPLIT:
         v = (variant & 0xF) or V_SPLIT
         if v != V_SPLIT:
@@ -434,6 +451,7 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
 
 def _maxdims_arg(stacked: StackedNetworks, dims=None) -> int:
     """Host int32[3] launch sizes, kept alive on the stacked object."""
+    ensure_finalized(stacked)
     dims = tuple(int(v) for v in (dims or stacked.maxdims))
     key = ("maxdims_host", dims)
     arr = stacked._cache.get(key)

@@ -22,7 +22,9 @@ import torch
 from . import _native
 from .config import NeatConfig
 from .device import device, ptr, stream_handle
-from .errors import ConfigError, CycleDetected, ShapeMismatch
+from dataclasses import dataclass
+
+from .errors import ConfigError, CycleDetected, ShapeMismatch, TerminalState
 from .functions import DEFAULT_REGISTRY, check_registry
 from .inference import (StackedNetworks, _check_codes, _check_status_codes, _maxdims_arg, _raise_cycles,
                         status_cyclic, transform_arrays)
@@ -44,6 +46,80 @@ def _xor_fitness(outputs: np.ndarray) -> np.ndarray:
 
 def _regression_fitness(outputs: np.ndarray, targets: np.ndarray) -> np.ndarray:
     return -((outputs[:, :, 0] - targets) ** 2).mean(axis=1)
+
+
+# ---------------------------------------------------------------------------
+# single-genome host entry points (problems.py:72-150): a user-supplied
+# forward callable, evaluated on the host one network at a time.  The
+# population path below runs the same fitness on the GPU.
+# ---------------------------------------------------------------------------
+
+def _as_column(outputs, n: int) -> np.ndarray:
+    y = np.asarray(outputs, dtype=np.float64)
+    if y.shape not in ((n, 1), (n,)):
+        raise ShapeMismatch(f"expected outputs of shape ({n}, 1), got {y.shape}")
+    return y.reshape(1, n, 1)
+
+
+def eval_xor(forward_fn) -> float:
+    """4 - sum of squared errors over the four XOR cases (problems.py:72-77)."""
+    return float(_xor_fitness(_as_column(forward_fn(XOR_INPUTS.copy()), 4))[0])
+
+
+def eval_regression(forward_fn, target_fn=np.sin, samples=None) -> float:
+    """-MSE against ``target_fn`` on the sample grid (problems.py:80-88)."""
+    xs = regression_grid(64) if samples is None else np.asarray(samples, dtype=np.float64)
+    y = _as_column(forward_fn(xs[:, None]), xs.size)
+    return float(_regression_fitness(y, target_fn(xs))[0])
+
+
+# cart-pole constants (problems.py:37-47); the device kernel (csrc/forward.cu
+# an_cartpole) integrates the same Euler step
+_G, _MC, _MP, _HL, _FORCE, _DT = 9.8, 1.0, 0.1, 0.5, 10.0, 0.02
+_X_LIMIT, _THETA_LIMIT = 2.4, 12 * 2 * math.pi / 360
+
+
+@dataclass(frozen=True)
+class CartPoleState:
+    """One cart-pole state (problems.py:93-104)."""
+    x: float
+    x_dot: float
+    theta: float
+    theta_dot: float
+    steps: int = 0
+
+    @property
+    def is_terminal(self) -> bool:
+        return abs(self.x) > _X_LIMIT or abs(self.theta) > _THETA_LIMIT or self.steps >= MAX_STEPS
+
+
+def cartpole_step(state: CartPoleState, force_direction: int) -> CartPoleState:
+    """One Euler step with force +-10 N: positions move with the old velocities,
+    then velocities with the accelerations (problems.py:107-135)."""
+    if force_direction not in (-1, 1):
+        raise ValueError(f"force_direction must be -1 or +1, got {force_direction}")
+    if state.is_terminal:
+        raise TerminalState("cart-pole state is already terminal")
+    f = float(force_direction) * _FORCE
+    c, s = math.cos(state.theta), math.sin(state.theta)
+    m = _MC + _MP
+    tmp = (f + _MP * _HL * state.theta_dot ** 2 * s) / m
+    th_acc = (_G * s - c * tmp) / (_HL * (4.0 / 3.0 - _MP * c ** 2 / m))
+    x_acc = tmp - _MP * _HL * th_acc * c / m
+    return CartPoleState(state.x + _DT * state.x_dot, state.x_dot + _DT * x_acc,
+                         state.theta + _DT * state.theta_dot, state.theta_dot + _DT * th_acc,
+                         state.steps + 1)
+
+
+def eval_cartpole(forward_fn, rng: RngStream) -> float:
+    """Steps survived (1..500) under the bang-bang policy sign(output) (problems.py:138-150)."""
+    u = np.asarray(rng.uniforms(4), dtype=np.float64).reshape(4) * 0.1 - 0.05
+    state = CartPoleState(*(float(v) for v in u))
+    while not state.is_terminal:
+        obs = np.array([state.x, state.x_dot, state.theta, state.theta_dot])
+        out = float(np.asarray(forward_fn(obs)).reshape(-1)[0])
+        state = cartpole_step(state, 1 if out > 0 else -1)
+    return float(state.steps)
 
 
 class Problem:
