@@ -156,14 +156,28 @@ def enabled_edges(nodes: np.ndarray, conns: np.ndarray) -> list[tuple[int, int, 
 
 def transform_genome(nodes: np.ndarray, conns: np.ndarray, num_inputs: int, num_outputs: int) -> dict:
     """Kahn order with the smallest ready ROW first, one node per step
-    (inference.py:114-141); cyclic if live nodes remain (:143)."""
+    (inference.py:114-141); cyclic if live nodes remain (:143).
+
+    Repeated (in, out) pairs follow the reference exactly: the dense incoming
+    row keeps the LAST conn row's weight (fancy assignment, :108-112), the
+    indegree counts every row (np.add.at, :114-115), and a picked source
+    decrements its successor once per distinct successor when max_nodes <= 64
+    (bitmask OR, :116-122,136-137) but once per row above that
+    (np.subtract.at, :139-141) -- so with <= 64 rows a repeated pair leaves its
+    destination unready and the genome reads as cyclic."""
     rows = key_to_row(nodes)
-    edges = enabled_edges(nodes, conns)
+    rows_edges = enabled_edges(nodes, conns)
+    last: dict[tuple[int, int], tuple[int, int, float, int]] = {}
+    for e in rows_edges:
+        last[(e[0], e[1])] = e
+    edges = sorted(last.values(), key=lambda e: e[3])
+    bitmask = nodes.shape[0] <= 64
     indeg = {r: 0 for r in rows.values()}
     succ: dict[int, list[int]] = {r: [] for r in rows.values()}
-    for s, d, _, _ in edges:
+    for s, d, _, _ in rows_edges:
         indeg[d] += 1
-        succ[s].append(d)
+        if not (bitmask and d in succ[s]):
+            succ[s].append(d)
     remaining = set(rows.values())
     order: list[int] = []
     while True:

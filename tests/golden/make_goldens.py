@@ -306,6 +306,49 @@ def make_evolution_goldens() -> None:
     _save("evolution.npz", **out)
 
 
+BIG_CFG = dict(EVO_CFG, inputs=32, outputs=8, max_nodes=128, max_conns=512, pop_size=48, conn_add=0.9,
+               compatibility_threshold=2.0, max_species=5)
+
+
+def make_big_evolution_goldens() -> None:
+    """mutate / reproduce at max_nodes 128 / max_conns 512 on genomes with > 64
+    live nodes: the reference's conn-add closure switches from the bitset
+    Warshall to float32 matmul squaring above 64 live rows (evolution.py:370-390)."""
+    from arrayneat.evolution import reproduce, speciate, update_stagnation, allocate_spawns
+    cfg = an.NeatConfig(**BIG_CFG)
+    nodes, conns = synthetic_population(160, 128, 512, 32, 8, seed=11, variant="M")
+    big = np.nonzero((~np.isnan(nodes[:, :, 0])).sum(axis=1) > 64)[0][:48]
+    nodes, conns = nodes[big], conns[big]
+    assert nodes.shape[0] == 48
+    P = nodes.shape[0]
+    out = {"nodes": nodes, "conns": conns}
+    for net in ("feedforward", "recurrent"):
+        mcfg = cfg.with_overrides(network_type=net)
+        st = an.RngStream(78).child(3, 2).split(np.arange(P))
+        st._counter = 3
+        keys = np.arange(1 << 21, (1 << 21) + P, dtype=np.float64)
+        mn, mc, added = an_evo.mutate_arrays(nodes, conns, mcfg, st, keys)
+        out[f"mut_{net}_nodes"], out[f"mut_{net}_conns"], out[f"mut_{net}_added"] = mn, mc, added
+        out[f"mut_{net}_counter"] = np.int64(st._counter)
+    fitness = np.round(np.random.default_rng(4).random(P) * 4.0, 1)
+    pop = an.PopulationTensors(nodes, conns, np.full(P, -1, np.int64), np.full(P, np.nan), 32, 8)
+    sp_pop, sp = speciate(pop, [], cfg)
+    out["spec_assigned"] = sp_pop.species_id
+    surv = update_stagnation(sp, fitness, cfg)
+    alloc = allocate_spawns(surv, fitness, cfg)
+    out["spawns"] = np.array([s.spawn_count for s in alloc])
+    allocator = an.NodeKeyAllocator(1 << 22)
+    off = reproduce(sp_pop, alloc, fitness, cfg, an.RngStream(14).child(4), allocator)
+    out["rep_nodes"], out["rep_conns"] = off.nodes, off.conns
+    out["rep_fitness"] = fitness
+    out["rep_next_key"] = np.int64(allocator.next_key)
+    _save("evolution_big.npz", **out)
+
+
+if __name__ == "__main__" and "big" in sys.argv:
+    make_big_evolution_goldens()
+
+
 def load_corpus() -> dict:
     with np.load(os.path.join(HERE, "corpus.npz")) as z:
         return {k: z[k] for k in z.files}

@@ -226,3 +226,46 @@ def test_slot_tables_device_ranking_equals_host(tn, monkeypatch):
     built = tn.evolution._slot_tables_device(species, fit, cfg)
     for a, b in zip(host, built):
         assert np.array_equal(a, b.cpu().numpy())
+
+
+# -- max_nodes 128 / max_conns 512 with > 64 live nodes: the reference's conn-add
+# closure is float32 matmul squaring there (evolution.py:370-390), the kernel's is
+# the bitset Warshall for every size (tests/golden/make_goldens.py BIG_CFG)
+
+def _big_cfg(tn, **kw):
+    return _cfg(tn, inputs=32, outputs=8, max_nodes=128, max_conns=512, pop_size=48, conn_add=0.9,
+                compatibility_threshold=2.0, max_species=5, **kw)
+
+
+@pytest.mark.parametrize("net", ["feedforward", "recurrent"])
+def test_mutate_arrays_128_512_over_64_live_nodes(tn, net):
+    from paper_2404_01817_b200.rng import RngStream
+    g = load_golden("evolution_big.npz")
+    p = g["nodes"].shape[0]
+    assert (~np.isnan(g["nodes"][:, :, 0])).sum(axis=1).min() > 64
+    st = RngStream(78).child(3, 2).split(np.arange(p))
+    st._counter = 3
+    mn, mc, added = tn.evolution.mutate_arrays(g["nodes"], g["conns"], _big_cfg(tn, network_type=net), st,
+                                               np.arange(1 << 21, (1 << 21) + p, dtype=np.float64))
+    assert st._counter == int(g[f"mut_{net}_counter"])
+    assert np.array_equal(added, g[f"mut_{net}_added"])
+    assert_genomes_match(mn, mc, g[f"mut_{net}_nodes"], g[f"mut_{net}_conns"])
+
+
+def test_reproduce_128_512_over_64_live_nodes(tn):
+    from paper_2404_01817_b200.rng import RngStream
+    g = load_golden("evolution_big.npz")
+    n, cc = g["nodes"], g["conns"]
+    p = n.shape[0]
+    cfg = _big_cfg(tn)
+    fitness = g["rep_fitness"]
+    pop = tn.PopulationTensors(n, cc, np.full(p, -1), np.full(p, np.nan), 32, 8)
+    sp_pop, sp = tn.evolution.speciate(pop, [], cfg)
+    assert np.array_equal(sp_pop.species_id, g["spec_assigned"])
+    surv = tn.evolution.update_stagnation(sp, fitness, cfg)
+    alloc = tn.evolution.allocate_spawns(surv, fitness, cfg)
+    assert [s.spawn_count for s in alloc] == list(g["spawns"])
+    allocator = tn.evolution.NodeKeyAllocator(1 << 22)
+    off = tn.evolution.reproduce(sp_pop, alloc, fitness, cfg, RngStream(14).child(4), allocator)
+    assert allocator.next_key == int(g["rep_next_key"])
+    assert_genomes_match(off.nodes, off.conns, g["rep_nodes"], g["rep_conns"])

@@ -43,8 +43,8 @@ def test_rng_split_and_sparse_cells_match_reference():
     assert np.array_equal(np.stack([s.uniforms(2) for s in streams]), g["split_after"])
 
 
-@pytest.mark.parametrize("name", ["forward_small.npz", "forward_cfg2_T.npz",
-                                  "forward_cfg2_M.npz", "corpus.npz"])
+@pytest.mark.parametrize("name", ["forward_small.npz", "forward_cfg2_T.npz", "forward_cfg2_M.npz",
+                                  "corpus.npz", "forward_dupes_n12.npz", "forward_dupes_n80.npz"])
 def test_transform_order_matches_reference(name):
     g = load_golden(name)
     n_in, n_out = int(g["num_inputs"]), int(g["num_outputs"])
@@ -61,8 +61,8 @@ def test_transform_order_matches_reference(name):
                                   equal_nan=True)
 
 
-@pytest.mark.parametrize("name", ["forward_small.npz", "forward_cfg2_T.npz",
-                                  "forward_cfg2_M.npz", "corpus.npz"])
+@pytest.mark.parametrize("name", ["forward_small.npz", "forward_cfg2_T.npz", "forward_cfg2_M.npz",
+                                  "corpus.npz", "forward_dupes_n12.npz", "forward_dupes_n80.npz"])
 def test_forward_matches_reference(name):
     g = load_golden(name)
     n_in, n_out = int(g["num_inputs"]), int(g["num_outputs"])

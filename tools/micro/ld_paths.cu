@@ -13,13 +13,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 template <int MODE, int BATCH>
 __global__ void __launch_bounds__(128) bench(const uint32_t* __restrict__ cols, int iters, float* out, long long* cyc) {
   __shared__ uint32_t tbase;
-  __shared__ __align__(16) float2 vals[40 * 128];
+  __shared__ __align__(16) float2 vals[32 * 128];
   const int warp = threadIdx.x >> 5;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(&tbase)) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  for (int i = threadIdx.x; i < 40 * 128; i += 128) vals[i] = make_float2(1.0f, 2.0f);
+  for (int i = threadIdx.x; i < 32 * 128; i += 128) vals[i] = make_float2(1.0f, 2.0f);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(128) bench(const uint32_t* __restrict__ cols, 
     uint32_t r[2 * BATCH];
 #pragma unroll
     for (int b = 0; b < BATCH; ++b) {
-      const uint32_t c = cols[(it * BATCH + b) & 255];
+      const uint32_t c = (uint32_t)(it * 5 + b * 7 + threadIdx.x / 32) & 31u;
       if (MODE == 0 || (MODE == 2 && b % 3 == 0)) {
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[2 * b]), "=r"(r[2 * b + 1]) : "r"(tm + 2 * c));
       } else if (MODE <= 2) {
@@ -79,8 +79,9 @@ int main() {
   uint32_t* cols; float* out; long long* cyc;
   cudaMalloc(&cols, sizeof(h)); cudaMemcpy(cols, h, sizeof(h), cudaMemcpyHostToDevice);
   cudaMalloc(&out, 148 * 8 * 128 * 4); cudaMalloc(&cyc, 148 * 8 * 8);
-  for (int occ : {1, 2, 4}) {
+  for (int occ : {2, 4, 6}) {
     run<0, 4>("tmem", 148 * occ, cols, out, cyc, 8000);
+    run<1, 4>("lds", 148 * occ, cols, out, cyc, 8000);
     run<0, 8>("tmem", 148 * occ, cols, out, cyc, 4000);
     run<1, 8>("lds", 148 * occ, cols, out, cyc, 4000);
     run<2, 6>("mix", 148 * occ, cols, out, cyc, 5000);
