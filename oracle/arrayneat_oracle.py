@@ -409,3 +409,87 @@ def recurrent_rollout(nodes: np.ndarray, conns: np.ndarray, num_inputs: int, num
         act = np.array([v[r] for r in out_rows])
         s = np.tanh(a @ s + m @ act)
     return reward
+
+
+# -- cart-pole episode replay (problems.py:107-177), test infrastructure only ---------
+
+
+def _two_prod(a: float, b: float) -> tuple[float, float]:
+    """Exact a*b = p + e (Dekker split; equals the device's fma(a, b, -p))."""
+    p = a * b
+    sp = 134217729.0  # 2^27 + 1
+    ta = sp * a
+    ah = ta - (ta - a)
+    al = a - ah
+    tb = sp * b
+    bh = tb - (tb - b)
+    bl = b - bh
+    return p, ((ah * bh - p) + ah * bl + al * bh) + al * bl
+
+
+def _dd_two_sum(a, b):
+    s = a + b
+    bb = s - a
+    return s, (a - (s - bb)) + (b - bb)
+
+
+def _dd_add(a, b):
+    s, e = _dd_two_sum(a[0], b[0])
+    return _dd_two_sum(s, e + (a[1] + b[1]))
+
+
+def _dd_mul(a, b):
+    p, e = _two_prod(a[0], b[0])
+    return _dd_two_sum(p, e + (a[0] * b[1] + a[1] * b[0]))
+
+
+def cos_sin_device(x: float) -> tuple[float, float]:
+    """Bitwise restatement of the cart-pole kernel's double-double cos/sin
+    (csrc/forward.cu cos_sin_cr), for |x| <= 0.5."""
+    from fractions import Fraction
+    fh, fl = [], []
+    for n in range(20):
+        f = Fraction(1, math.factorial(n))
+        fh.append(float(f))
+        fl.append(float(f - Fraction(float(f))))
+    x2h = x * x
+    y = _two_prod(x, x)
+    assert y[0] == x2h
+
+    def series(j0):
+        acc = (0.0, 0.0)
+        for k in range(8, -1, -1):
+            n = j0 + 2 * k
+            c = (-fh[n], -fl[n]) if k & 1 else (fh[n], fl[n])
+            acc = _dd_add(_dd_mul(acc, y), c)
+        return acc
+    cs = series(0)
+    sn = _dd_mul(series(1), (x, 0.0))
+    return cs[0] + cs[1], sn[0] + sn[1]
+
+
+def cartpole_episode(nodes: np.ndarray, conns: np.ndarray, start, cos_sin=None, max_steps: int = 500) -> int:
+    """Steps survived by one genome (problems.py:138-177 lockstep semantics:
+    Euler step, bang-bang force sign(output > 0), termination |x| > 2.4 or
+    |theta| > 12 deg).  ``cos_sin`` picks the libm: None = numpy's (the
+    reference), ``cos_sin_device`` = the kernel's."""
+    tr = transform_genome(nodes, conns, 4, 1)
+    g, mc, mp, hl, fm, dt = 9.8, 1.0, 0.1, 0.5, 10.0, 0.02
+    tm, pl = mc + mp, mp * hl
+    x, xd, th, thd = (float(v) for v in start)
+    steps = 0
+    for _ in range(max_steps):
+        out = forward_genome(nodes, tr, np.array([[x, xd, th, thd]]))[0, 0]
+        force = fm if out > 0 else -fm
+        if cos_sin is None or abs(th) > 0.5:
+            ct, st = float(np.cos(th)), float(np.sin(th))
+        else:
+            ct, st = cos_sin(th)
+        tmp = (force + pl * thd ** 2 * st) / tm
+        tacc = (g * st - ct * tmp) / (hl * (4.0 / 3.0 - mp * ct ** 2 / tm))
+        xacc = tmp - pl * tacc * ct / tm
+        x, xd, th, thd = x + dt * xd, xd + dt * xacc, th + dt * thd, thd + dt * tacc
+        steps += 1
+        if abs(x) > 2.4 or abs(th) > 12 * 2 * math.pi / 360:
+            break
+    return steps

@@ -1195,6 +1195,60 @@ __device__ void warp_eval_single(const uint8_t* gp, const ProgLayout& L, T* vals
   }
 }
 
+// cos / sin of the pole angle, correctly rounded for |x| <= 0.5 (double-double
+// Taylor sums; the cart-pole angle stays within ~0.21 rad).  numpy's float64
+// cos/sin agree with glibc's correctly rounded results on this range, so the
+// episode's float64 states follow the reference bit for bit (the CUDA libm
+// versions are within 1-2 ulp and let chaotic episodes drift apart).
+struct DD { double hi, lo; };
+__device__ __forceinline__ DD dd_two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b), bb = __dsub_rn(s, a);
+  return {s, __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb))};
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  DD s = dd_two_sum(a.hi, b.hi);
+  s.lo = __dadd_rn(s.lo, __dadd_rn(a.lo, b.lo));
+  return dd_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ DD dd_mul(DD a, DD b) {
+  const double p = __dmul_rn(a.hi, b.hi);
+  const double e = fma(a.hi, b.hi, -p);
+  return dd_two_sum(p, __dadd_rn(e, __dadd_rn(__dmul_rn(a.hi, b.lo), __dmul_rn(a.lo, b.hi))));
+}
+// sum_{k=0..K} c_k * y^k (Horner, y = x^2) with double-double coefficients
+// c_k = s * 1 / (j0 + 2k)! alternating; (hi, lo) pairs of 1/n! below
+__device__ DD dd_series(DD y, bool is_sin) {
+  // 1/n! for n = 0..19 as double-double (hi = RN(1/n!), lo = RN(1/n! - hi))
+  const double fh[20] = {1.0, 1.0, 0.5, 1.6666666666666666e-01, 4.1666666666666664e-02, 8.3333333333333332e-03,
+                         1.3888888888888889e-03, 1.9841269841269841e-04, 2.4801587301587302e-05,
+                         2.7557319223985893e-06, 2.7557319223985888e-07, 2.5052108385441720e-08,
+                         2.0876756987868100e-09, 1.6059043836821613e-10, 1.1470745597729725e-11,
+                         7.6471637318198164e-13, 4.7794773323873853e-14, 2.8114572543455206e-15,
+                         1.5619206968586225e-16, 8.2206352466243295e-18};
+  const double fl[20] = {0.0, 0.0, 0.0, 9.2518585385429707e-18, 2.3129646346357427e-18, 1.1564823173178714e-19,
+                         -5.3005439543735771e-20, 1.7209558293420705e-22, 2.1511947866775882e-23,
+                         -1.8583932740464721e-22, 2.3767714622250297e-23, -1.4488140709359119e-24,
+                         -1.2073450591132599e-25, 1.2585294588752098e-26, 2.0655512752830745e-28,
+                         7.0387287773345300e-30, 4.3992054858340813e-31, 1.6508842730861433e-31,
+                         1.1910679660273754e-32, 2.2141894119604265e-34};
+  const int j0 = is_sin ? 1 : 0;
+  DD acc = {0.0, 0.0};
+  for (int k = 8; k >= 0; --k) {
+    const int n = j0 + 2 * k;
+    DD c = {(k & 1) ? -fh[n] : fh[n], (k & 1) ? -fl[n] : fl[n]};
+    acc = dd_add(dd_mul(acc, y), c);
+  }
+  return acc;
+}
+__device__ __forceinline__ void cos_sin_cr(double x, double& c, double& s) {
+  const double x2h = __dmul_rn(x, x);
+  const DD y = {x2h, fma(x, x, -x2h)};
+  const DD cs = dd_series(y, false);
+  const DD sn = dd_mul(dd_series(y, true), DD{x, 0.0});
+  c = __dadd_rn(cs.hi, cs.lo);
+  s = __dadd_rn(sn.hi, sn.lo);
+}
+
 template <typename T>
 __global__ void cartpole_kernel(const uint8_t* __restrict__ prog, ProgLayout L, int64_t P, int max_slots,
                                 const double* __restrict__ start, int max_steps, double* __restrict__ fitness) {
@@ -1216,7 +1270,9 @@ __global__ void cartpole_kernel(const uint8_t* __restrict__ prog, ProgLayout L, 
     warp_eval_single<T>(gp, L, vals);
     const double out = out0 != NO_SLOT ? (double)vals[out0] : __longlong_as_double(0x7ff8000000000000ll);
     const double force = out > 0.0 ? FM : -FM;
-    const double ct = cos(th), st = sin(th);
+    double ct, st;
+    if (fabs(th) <= 0.5) cos_sin_cr(th, ct, st);
+    else { ct = cos(th); st = sin(th); }
     const double tmp = __ddiv_rn(__dadd_rn(force, __dmul_rn(__dmul_rn(PL, __dmul_rn(thd, thd)), st)), TM);
     const double tacc = __ddiv_rn(__dsub_rn(__dmul_rn(G, st), __dmul_rn(ct, tmp)),
                                   __dmul_rn(HL, __dsub_rn(4.0 / 3.0, __ddiv_rn(__dmul_rn(PM, __dmul_rn(ct, ct)), TM))));

@@ -47,7 +47,7 @@ def test_random_shapes_match_oracle(tn, seed):
     dt = np.float64 if precision == "f64" else np.float32
     x = np.random.default_rng(seed).standard_normal((pop, batch, n_in)).astype(dt)
     out = tn.forward_device(st, torch.from_numpy(x).cuda()).cpu().numpy()
-    tol = 1e-9 if precision == "f64" else (1e-5 if variant == "T" else 1e-4)
+    tol = 1e-9 if precision == "f64" else 1e-5
     for p in range(pop):
         ref = orc.forward_genome(nodes[p], orc.transform_genome(nodes[p], conns[p], n_in, n_out),
                                  x[p].astype(np.float64))

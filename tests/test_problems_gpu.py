@@ -34,9 +34,28 @@ def test_problem_fitness(tn, name, ni):
     fit = tn.make_problem(cfg).evaluate_population_tensors(pop, rng=tn.RngStream(9).child(4, 1))
     ref = g[f"{name}_fitness"]
     if name == "cartpole":
-        assert np.mean(fit == ref) >= 0.97, np.nonzero(fit != ref)
+        _check_cartpole(g, fit, ref)
     else:
         np.testing.assert_allclose(fit, ref, rtol=1e-9, atol=1e-9)
+
+
+def _check_cartpole(g, fit, ref):
+    """Episodes are step-exact against the reference.  The only admissible
+    difference is libm rounding of cos/sin (the kernel's double-double cos/sin
+    vs numpy's, which can differ by 1 ulp near a rounding midpoint, and a
+    chaotic episode can amplify that): each mismatching genome must be
+    reproduced exactly by host replays of the same episode -- numpy's cos/sin
+    giving the reference's step count and the kernel's cos/sin giving ours
+    (oracle.cartpole_episode; start states = the reference's per-genome
+    streams RngStream(9).child(4, 1).split(i).uniforms(4), problems.py:157)."""
+    from oracle import arrayneat_oracle as orc
+    nodes, conns = g["cartpole_nodes"], g["cartpole_conns"]
+    bad = np.nonzero(fit != ref)[0]
+    assert bad.size <= 3, bad
+    for p in list(bad) + [0, 1, 2]:
+        start = orc.Stream(orc.stream_key(9, 4, 1, int(p))).uniforms(4) * 0.1 - 0.05
+        assert orc.cartpole_episode(nodes[p], conns[p], start) == ref[p], p
+        assert orc.cartpole_episode(nodes[p], conns[p], start, orc.cos_sin_device) == fit[p], p
 
 
 def test_xor_problem_fp32_path(tn):
@@ -45,7 +64,10 @@ def test_xor_problem_fp32_path(tn):
     prob.precision = "f32"
     pop = tn.PopulationTensors(g["xor_nodes"], g["xor_conns"], None, None, 2, 1)
     fit = prob.evaluate_population_tensors(pop)
-    np.testing.assert_allclose(fit, g["xor_fitness"], rtol=0, atol=1e-4)
+    # fitness = 4 - sum_b (y_b - t_b)^2 over 4 cases: |d fit| <= 2 sum |y - t| |d y| <= 8e-5 for
+    # outputs within north_star's 1e-5; measured well inside 1e-5 * max(1, |fit|)
+    ref = g["xor_fitness"]
+    assert np.max(np.abs(fit - ref) / np.maximum(1.0, np.abs(ref))) <= 1e-5
 
 
 def test_short_xor_run_tracks_reference(tn):
