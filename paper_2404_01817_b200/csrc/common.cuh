@@ -89,31 +89,20 @@ template <> struct __align__(16) StepT<double> {
 // arrays, u16 source slots and f32 weights (6 bytes per edge)
 struct __align__(16) EdgeD { uint32_t src; uint32_t pad; double w; };
 
-// Split programs (format bit FMT_SPLIT, fp32 feed-forward; forward.cu
-// fwd_split_kernel): input values live in tensor memory, hidden values in
-// shared-memory slots numbered from 0 (inputs take no slot).  Each group has
-// two interleaved edge blocks with the GroupRec layout: the input block
-// (source = input key, a TMEM column group; holes read input 0 with weight
-// 0) and the hidden block (source = hidden slot; holes read the zero slot).
-// Sum/mean groups pad both blocks to even rounds; non-sum steps are
-// singletons with exact counts in both blocks.
-struct __align__(16) GroupSplit {  // 32 bytes
-  uint8_t n;
-  uint8_t cls;
-  uint16_t step_begin;
-  uint16_t rounds_in;  // input block rounds
-  uint16_t e_in;       // first input-block entry (multiple of 8)
-  uint16_t rounds_h;   // hidden block rounds
-  uint16_t e_h;        // first hidden-block entry (multiple of 8)
-  uint16_t pad[2];
-  uint16_t cnt_in[4];  // input edges of each step
-  uint16_t cnt_h[4];   // hidden edges of each step
-};
-
-enum : int { FMT_F64 = 1, FMT_SPLIT = 2 };
+// Program format bits.  FMT_TC (fp32 feed-forward): programs whose steps all
+// aggregate by sum / mean get the tensor-core input layer (forward.cu
+// fwd_tc_kernel, csrc/digits.cuh): the input-sourced part of every step is one
+// digit-split MMA per 128-sample tile, and the group / step / edge areas hold
+// the hidden-sourced edges only, with one value slot per step (slot = step
+// index, zero slot = n_steps).  Appended areas: per-step column factors, the
+// input edge lists (exact path for rows the MMA cannot scale) and the B
+// operand (digit planes, UMMA K-major layout).  Other genomes of an FMT_TC
+// population get standard programs in the same stride (ProgHeader.mode = 0
+// instead of MODE_TC).
+enum : int { FMT_F64 = 1, FMT_TC = 2 };
+enum : int { MODE_FF = 0, MODE_REC = 1, MODE_TC = 2 };
 
 static_assert(sizeof(GroupRec) == 16, "group layout");
-static_assert(sizeof(GroupSplit) == 32, "group layout");
 static_assert(sizeof(StepT<float>) == 16, "step layout");
 static_assert(sizeof(StepT<double>) == 32, "step layout");
 static_assert(sizeof(EdgeD) == 16, "edge layout");
@@ -125,22 +114,60 @@ __host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + 
 // <= 8/3 x real), rounds are even (+gw <= 4 per group) and every group starts
 // on a multiple of 8 (+7)
 __host__ __device__ inline int64_t edge_capacity(int N, int C) { return 3ll * C + 12ll * N + 16; }
-// split programs: input blocks obey the bound above; a hidden block is padded
-// to its longest list (<= 4x real); both blocks round and align per group
-__host__ __device__ inline int64_t edge_capacity_split(int N, int C) { return 7ll * C + 24ll * N + 16; }
 
 struct ProgLayout {
   int64_t off_out, off_groups, off_steps, off_src, off_w, stride;
+  // FMT_TC: a MODE_TC program keeps everything the tensor-core kernel stages in
+  // one contiguous block at off_tc (internal offsets from the genome's counts,
+  // tc_block), and the exact-path input edge lists at fixed offsets; its
+  // standard areas (off_groups..) are unused.  0 for other formats.
+  int64_t off_tc, off_in, off_isrc, off_iw;
 };
 
-// `precision` is the program format: bit 0 = fp64 program, bit 1 = split layout (fp32)
+// TC group record (pre-decoded for the sweep): code = (n - 1) | tanh << 2 |
+// split0 << 3 (the dispatch index), rounds, first edge entry, first step.  In
+// tanh groups the step records carry bias and response pre-multiplied by
+// -2 log2(e) (the epilogue's EX2 argument is one FFMA away)
+struct __align__(16) GroupTC {
+  uint32_t code, rounds, e_begin, step_begin;
+};
+static_assert(sizeof(GroupTC) == 16, "group layout");
+constexpr float TANH_K = -2.8853900817779268f;
+
+constexpr int TC_SAMPLES = 256;            // samples per tile of the tensor-core kernel
+constexpr int TC_SLOT_BYTES = TC_SAMPLES * 4;  // one value slot row [128 threads][2 samples] fp32
+
+__host__ __device__ inline int tc_rows(int n) { return (n + 15) / 16 * 16; }
+
+// the staged block of a MODE_TC program: B operand (round16(steps) rows x 192 B,
+// UMMA K-major core matrices, csrc/digits.cuh), column factors f32[nb], group
+// records, step records, hidden-edge source byte offsets u32 (slot *
+// TC_SLOT_BYTES) and weights f32 (the look-ahead of the word prefetch reads
+// past the weights: the kernel leaves slack after the block)
+struct TcBlock {
+  uint32_t b, cf, gr, st, src, w, bytes;
+};
+__host__ __device__ inline TcBlock tc_block(int n_steps, int n_groups, int n_edges) {
+  TcBlock t;
+  const uint32_t nb = (uint32_t)tc_rows(n_steps);
+  t.b = 0;
+  t.cf = 192u * nb;
+  t.gr = t.cf + 4u * nb;
+  t.st = t.gr + 16u * (uint32_t)n_groups;
+  t.src = t.st + 16u * (uint32_t)n_steps;
+  t.w = t.src + 4u * (uint32_t)n_edges;
+  t.bytes = (t.w + 4u * (uint32_t)n_edges + 15u) & ~15u;
+  return t;
+}
+
+// `precision` is the program format: bit 0 = fp64 program, bit 1 = FMT_TC (fp32)
 __host__ __device__ inline ProgLayout prog_layout(int N, int C, int O, int precision) {
   ProgLayout L;
-  const bool split = (precision & FMT_SPLIT) != 0;
-  const int64_t E = split ? edge_capacity_split(N, C) : edge_capacity(N, C);
+  const int64_t E = edge_capacity(N, C);
   L.off_out = 32;
   L.off_groups = align_up(L.off_out + 2 * (int64_t)O, 16);
-  L.off_steps = align_up(L.off_groups + (split ? 32ll : 16ll) * N, 16);
+  L.off_steps = align_up(L.off_groups + 16ll * N, 16);
+  L.off_tc = L.off_in = L.off_isrc = L.off_iw = 0;
   if (precision & FMT_F64) {
     L.off_src = align_up(L.off_steps + 32ll * N, 16);
     L.off_w = L.off_src;  // EdgeD pairs
@@ -149,6 +176,15 @@ __host__ __device__ inline ProgLayout prog_layout(int N, int C, int O, int preci
     L.off_src = align_up(L.off_steps + 16ll * N, 16);
     L.off_w = align_up(L.off_src + 2 * E, 16);
     L.stride = align_up(L.off_w + 4 * E, 16);
+    if (precision & FMT_TC) {
+      const int64_t Cc = C > 0 ? C : 1;
+      L.off_tc = align_up(L.off_out + 2 * (int64_t)O, 128);
+      L.off_in = align_up(L.off_tc + tc_block(N, N, (int)E).bytes, 16);
+      L.off_isrc = align_up(L.off_in + 2ll * (N + 1), 16);
+      L.off_iw = align_up(L.off_isrc + 2 * Cc, 16);
+      const int64_t end = align_up(L.off_iw + 4 * Cc, 128);
+      L.stride = end > align_up(L.stride, 128) ? end : align_up(L.stride, 128);
+    }
   }
   return L;
 }

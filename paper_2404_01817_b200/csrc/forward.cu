@@ -19,8 +19,9 @@
 //     For small batches (XOR B=4, regression B=64, cart-pole B=1) where a
 //     thread-per-input mapping would idle most lanes.  Optionally fuses the
 //     XOR / regression fitness epilogue (problems.py:54-61).
-//   * fwd_split (split programs, opt-in): input values in tensor memory
-//     (tcgen05.st / tcgen05.ld), hidden values in shared memory.
+//   * fwd_tc (FMT_TC programs, config 2's default): the input-sourced edges
+//     of every step as one exact digit-split tcgen05 MMA per 128-sample tile
+//     (csrc/digits.cuh), the hidden-sourced edges swept on CUDA cores.
 //
 // Semantics: input rows hold raw inputs and are never
 // activated; node = act(bias + response * agg(w * v)); empty aggregation = 0;
@@ -28,6 +29,9 @@
 
 #include "common.cuh"
 #include "tc.cuh"
+#include "digits.cuh"
+#include "tmap.cuh"
+#include <cuda_fp16.h>
 
 namespace tneat {
 
@@ -178,7 +182,9 @@ __device__ __forceinline__ void sum_round1(float2 (&acc)[G][(S + 1) / 2], const 
 // tanh/sum (short epilogue).
 // MERGE (GRP_SPLIT0 groups of 3 steps): G = 4 columns, column 3 continues
 // step 0 and is added into it before the epilogue
-template <int S, int G, int RB, bool TANH, bool MERGE = false>
+// INIT (TC programs): every step owns slot step_begin + j, which holds the
+// step's input-layer partial sum on entry (the accumulator's initial value)
+template <int S, int G, int RB, bool TANH, bool MERGE = false, bool INIT = false>
 __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t* __restrict__ off_s,
                                               const float* __restrict__ w_s,
                                               const StepT<float>* __restrict__ st, char* vb, Words& wd,
@@ -192,6 +198,14 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
   for (int j = 0; j < G; ++j)
 #pragma unroll
     for (int p = 0; p < SP; ++p) acc[j][p] = make_float2(0.0f, 0.0f);
+  if constexpr (INIT) {
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const PackT v = *reinterpret_cast<const PackT*>(vb + (uint32_t)(gr.step_begin + j) * RB);
+#pragma unroll
+      for (int p = 0; p < SP; ++p) acc[j][p] = make_float2(v.v[2 * p], S > 2 * p + 1 ? v.v[(2 * p + 1) % S] : 0.0f);
+    }
+  }
   // step records are read up front so the epilogue does not wait on them
   uint32_t slot_j[G];
   float rk_j[G], bk_j[G];
@@ -200,9 +214,9 @@ __device__ __forceinline__ void run_sum_group(const GroupRec& gr, const uint32_t
 #pragma unroll
     for (int j = 0; j < NS; ++j) {
       const StepT<float> sj = st[j];
-      slot_j[j] = sj.slot;
-      rk_j[j] = sj.resp * K;
-      bk_j[j] = sj.bias * K;
+      slot_j[j] = INIT ? (uint32_t)(gr.step_begin + j) : sj.slot;
+      rk_j[j] = INIT ? sj.resp : sj.resp * K;  // TC programs store them pre-scaled (common.cuh GroupTC)
+      bk_j[j] = INIT ? sj.bias : sj.bias * K;
     }
   }
   const uint32_t* op = off_s + gr.e_begin;
@@ -668,377 +682,469 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
 }
 
 // ---------------------------------------------------------------------------
-// split-program forward: input values in tensor memory, hidden values in
-// shared memory
+// tensor-core forward (FMT_TC programs): input layer on tcgen05, hidden
+// edges on CUDA cores
 // ---------------------------------------------------------------------------
 //
-// One CTA of 128 threads (4 warps; warp w owns TMEM lanes 32w..32w+31) per
-// (genome, run of `tpc` tiles of 128*S inputs).  Thread t owns samples
-// t*S..t*S+S-1: it loads its own input rows (16-byte loads, L2-prefetched by the
-// TMA engine), stores them to its TMEM lane (column k*S + s = input k of sample
-// s; tcgen05.st) and reads them back per input edge with one tcgen05.ld of S
-// columns.  Only the hidden values occupy shared memory ([slot][128*S + S]),
-// so a CTA needs roughly a third of the tile kernel's shared memory per input
-// and more warps stay resident.  Every value a thread reads it wrote itself
-// (TMEM lane / shared column), so the tile loop has no CTA barrier.
-// Input-block holes read input 0 with weight 0; a tile whose inputs are not all
-// finite runs the exact variant that skips holes (inf * 0 would be NaN).
-#ifndef TNEAT_SPLIT_WARPS
-#define TNEAT_SPLIT_WARPS 24
+// Persistent: one CTA per SM with W warpgroups (4 warps each, W <= 4 as shared
+// memory allows).  The CTA walks its genomes (blockIdx.x, + gridDim.x, ...);
+// each genome's staged block (B operand, column factors, group / step records,
+// hidden edges: common.cuh tc_block) arrives by one bulk copy into one of two
+// buffers -- the next genome's copy is in flight while the current one runs --
+// and the warpgroups share it, warpgroup w taking tiles w, w + W, ... of 256
+// samples.  Thread r of a warpgroup owns samples r and r + 128 of its tile
+// (TMEM lane r of the two MMA halves; warp w%4 reads lanes 32(w%4)..), two
+// samples per thread so the sweep's warp-uniform work (program words, group
+// records, dispatch) and its packed FFMA2 arithmetic cover 64 samples.  Per
+// tile, within the warpgroup (named barrier 1 + w):
+//   1. the (256 x 32) fp32 input block lands by TMA (3-D tensor map, 128-byte
+//      swizzle, zero fill past B and past I) in the warpgroup's area;
+//   2. each thread reads its two rows into registers, block-scales them by a
+//      power of two and writes three fp16 digit planes over the same area
+//      (A operand, two 128-row halves, K-major core matrices;
+//      csrc/digits.cuh);
+//   3. one thread takes a TMEM column slot (2 halves x D4 / D32 x nb columns;
+//      the CTA's 512 columns are shared by its warpgroups through a bitmask)
+//      and issues 2 x 12 kind::f16 MMAs against the genome's B operand;
+//   4. each thread reads its TMEM lane and writes every step's input partial
+//      sums (both samples) into the step's value slot ([slot][128][2] fp32,
+//      over the consumed A area), then the slot is released;
+//   5. the hidden-edge sweep (the tile kernel's group records) starts each
+//      step's accumulator from its slot, and the outputs are stored.
+// Rows whose scale is out of range (non-finite inputs, |x| >= 2^62 or a
+// nonzero max < 2^-62) get zero digits and an exact fp32 partial from the
+// program's input edge lists instead.
+constexpr int TC_NT = 128;                   // threads per warpgroup = rows per MMA half
+constexpr int TC_TT = TC_SAMPLES;            // samples per tile
+constexpr int TC_RB = TC_SLOT_BYTES;         // bytes of one value slot row
+constexpr int TC_IN_BYTES = TC_TT * 128;     // fp32 input tile, 256 rows x 128 B
+constexpr int TC_A_HALF = TC_NT * TC_ROWB;   // A operand of one 128-row half: 24 KB
+constexpr int TC_MAX_WG = 4;
+static_assert(TC_TT == 2 * TC_NT, "two samples per thread");
+
+// per-warpgroup area: A operand / value slots from the start, the input tile
+// at the end (>= 48 KB, 1024-aligned: TMA 128-byte swizzle)
+__host__ __device__ inline uint32_t tc_wg_bytes(int nb) {
+  int64_t u = (int64_t)(nb + 1) * TC_RB;
+  if (u < 2 * TC_A_HALF) u = 2 * TC_A_HALF;
+  if (u < TC_IN_BYTES) u = TC_IN_BYTES;
+  return (uint32_t)align_up(u, 1024);
+}
+
+__device__ __forceinline__ void run_group_tc(const uint4 rec, const uint32_t* src_s, const float* w_s,
+                                             const StepT<float>* st_all, char* vb, Words& wd, int next_e) {
+  constexpr int S = 2, RB = TC_RB;
+  GroupRec gr;  // the fields run_sum_group reads (TC group records are pre-decoded: common.cuh GroupTC)
+  gr.rounds = (uint16_t)rec.y;
+  gr.e_begin = (uint16_t)rec.z;
+  gr.step_begin = (uint16_t)rec.w;
+  const StepT<float>* st = st_all + rec.w;
+  switch (rec.x) {
+    case 0: run_sum_group<S, 1, RB, false, false, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
+    case 1: run_sum_group<S, 2, RB, false, false, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
+    case 2: run_sum_group<S, 3, RB, false, false, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
+    case 3: run_sum_group<S, 4, RB, false, false, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
+    case 4: run_sum_group<S, 1, RB, true, false, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
+    case 5: run_sum_group<S, 2, RB, true, false, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
+    case 6: run_sum_group<S, 3, RB, true, false, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
+    case 7: run_sum_group<S, 4, RB, true, false, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
+    case 10: run_sum_group<S, 4, RB, false, true, true>(gr, src_s, w_s, st, vb, wd, next_e); break;
+    default: run_sum_group<S, 4, RB, true, true, true>(gr, src_s, w_s, st, vb, wd, next_e); break;  // 14
+  }
+}
+
+// the 2 x 12 MMAs of a tile, from one elected lane of a converged warp whose
+// operands are warp-uniform (shuffled from lane 0): the compiler keeps them in
+// uniform registers (no per-MMA broadcast loop)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 %%rx;\n.reg .pred %%px;\nelect.sync %%rx|%%px, %1;\n@%%px mov.s32 %0, 1;\n}\n"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
+}
+
+__device__ __forceinline__ void tc_issue_mmas(uint32_t a_addr, uint32_t b_addr, uint32_t dcol, int nb,
+                                              uint32_t bar) {
+  const uint32_t idesc = idesc_f16(TC_NT, nb);
+  if (elect_one()) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t ah = a_addr + (uint32_t)(h * TC_A_HALF);
+      auto A = [&](int k0) { return smem_desc(ah + (uint32_t)(k0 >> 3) * TC_LBO, TC_SBO, TC_LBO); };
+      auto Bd = [&](int k0) { return smem_desc(b_addr + (uint32_t)(k0 >> 3) * TC_LBO, TC_SBO, TC_LBO); };
+      const uint32_t d4 = dcol + (uint32_t)(2 * h * nb), d32 = d4 + (uint32_t)nb;
+#ifndef TNEAT_DIAG_TC_NOMMA  // diagnostic builds only: commit without MMAs
+      mma_f16(d4, A(0), Bd(0), idesc, 0u);  // D4 = A2 B2
+      mma_f16(d4, A(16), Bd(16), idesc, 1u);
+      mma_f16(d32, A(0), Bd(64), idesc, 0u);  // class 2 = A2 B0 + A1 B1 + A0 B2
+      mma_f16(d32, A(16), Bd(80), idesc, 1u);
+      mma_f16(d32, A(32), Bd(32), idesc, 1u);
+      mma_f16(d32, A(48), Bd(48), idesc, 1u);
+      mma_f16(d32, A(64), Bd(0), idesc, 1u);
+      mma_f16(d32, A(80), Bd(16), idesc, 1u);
+      mma_f16_scale10(d32, A(0), Bd(32), idesc);  // * 2^-10, + class 3 = A2 B1 + A1 B2
+      mma_f16(d32, A(16), Bd(48), idesc, 1u);
+      mma_f16(d32, A(32), Bd(0), idesc, 1u);
+      mma_f16(d32, A(48), Bd(16), idesc, 1u);
 #endif
-constexpr int SPLIT_NT = 128;
-
-__device__ __forceinline__ GroupSplit decode_group(const GroupSplit* gs, int g) {
-  const uint4 a = reinterpret_cast<const uint4*>(gs)[2 * g];
-  const uint4 b = reinterpret_cast<const uint4*>(gs)[2 * g + 1];
-  GroupSplit gr;
-  gr.n = (uint8_t)(a.x & 0xFF);
-  gr.cls = (uint8_t)((a.x >> 8) & 0xFF);
-  gr.step_begin = (uint16_t)(a.x >> 16);
-  gr.rounds_in = (uint16_t)(a.y & 0xFFFF);
-  gr.e_in = (uint16_t)(a.y >> 16);
-  gr.rounds_h = (uint16_t)(a.z & 0xFFFF);
-  gr.e_h = (uint16_t)(a.z >> 16);
-  gr.cnt_in[0] = (uint16_t)(b.x & 0xFFFF);
-  gr.cnt_in[1] = (uint16_t)(b.x >> 16);
-  gr.cnt_in[2] = (uint16_t)(b.y & 0xFFFF);
-  gr.cnt_in[3] = (uint16_t)(b.y >> 16);
-  gr.cnt_h[0] = (uint16_t)(b.z & 0xFFFF);
-  gr.cnt_h[1] = (uint16_t)(b.z >> 16);
-  gr.cnt_h[2] = (uint16_t)(b.w & 0xFFFF);
-  gr.cnt_h[3] = (uint16_t)(b.w >> 16);
-  return gr;
+    }
+    mma_commit(bar);
+  }
+  __syncwarp();
 }
 
-// input-block helpers: issue the TMEM loads of two rounds (up to 2*GW loads of
-// S columns; holes load input 0), and the FMAs once they have landed.
-// EXACT: entries past a step's count are skipped (non-finite inputs).
-template <int S, int G, int GW>
-__device__ __forceinline__ void input_issue(float (&v)[2 * GW * S], const uint32_t (&col)[2 * GW], uint32_t tlane,
-                                            uint32_t cmask) {
+// one input row -> registers (128-byte swizzle: chunk c of row r at c ^ (r & 7))
+__device__ __forceinline__ void tc_load_row(const uint8_t* rowp, int r, float (&x)[TC_K]) {
 #pragma unroll
-  for (int q = 0; q < 2 * GW; ++q)
-    if (q % GW < G) tmem_ld_cols<S>(tlane + col[q], v + q * S);  // columns < the allocation by construction
-}
-template <int S, int G, int GW, bool EXACT>
-__device__ __forceinline__ void input_fma(float2 (&acc)[G][(S + 1) / 2], const float (&v)[2 * GW * S],
-                                          const float (&w)[2 * GW], int r, const uint16_t (&cnt)[4]) {
-#pragma unroll
-  for (int q = 0; q < 2 * GW; ++q)
-    if (q % GW < G && (!EXACT || r + q / GW < cnt[q % GW])) {
-      if constexpr (S == 1) {
-        acc[q % GW][0].x = fmaf(w[q], v[q], acc[q % GW][0].x);
-      } else {
-#pragma unroll
-        for (int p = 0; p < S / 2; ++p)
-          acc[q % GW][p] = __ffma2_rn(make_float2(w[q], w[q]), make_float2(v[q * S + 2 * p], v[q * S + 2 * p + 1]),
-                                      acc[q % GW][p]);
-      }
-    }
-}
-
-template <int S, int G, int RB, bool TANH, bool EXACT>
-__device__ __forceinline__ void run_split_group(const GroupSplit& gr, const uint32_t* __restrict__ off_s,
-                                                const float* __restrict__ w_s, const StepT<float>* __restrict__ st,
-                                                char* vb, uint32_t tlane, uint32_t cmask) {
-  constexpr int GW = G == 3 ? 4 : G;
-  constexpr int SP = (S + 1) / 2;
-  using PackT = Pack<float, S>;
-  float2 acc[G][SP];
-#pragma unroll
-  for (int j = 0; j < G; ++j)
-#pragma unroll
-    for (int p = 0; p < SP; ++p) acc[j][p] = make_float2(0.0f, 0.0f);
-  // step records are read up front so the epilogue does not wait on them
-  uint32_t slot_j[G];
-  float rk_j[G], bk_j[G];
-  if constexpr (TANH) {
-    constexpr float K = -2.8853900817779268f;
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const StepT<float> sj = st[j];
-      slot_j[j] = sj.slot;
-      rk_j[j] = sj.resp * K;
-      bk_j[j] = sj.bias * K;
-    }
-  }
-  {  // input block: TMEM columns, two rounds per wait::ld
-    const uint32_t* op = off_s + gr.e_in;
-    const float* wp = w_s + gr.e_in;
-#pragma unroll 1
-    for (int r = 0; r < gr.rounds_in; r += 2) {
-      uint32_t c[2 * GW];
-      float w[2 * GW];
-      float v[2 * GW * S];
-      load_u32<2 * GW>(op + r * GW, c);
-      load_f32<2 * GW>(wp + r * GW, w);
-      input_issue<S, G, GW>(v, c, tlane, cmask);
-      tmem_wait_ld(v);
-      input_fma<S, G, GW, EXACT>(acc, v, w, r, gr.cnt_in);
-    }
-  }
-  {  // hidden block: shared-memory slots, double-buffered program words
-    const uint32_t* op = off_s + gr.e_h;
-    const float* wp = w_s + gr.e_h;
-    const int rounds = gr.rounds_h;
-    uint32_t oa[2 * GW], ob[2 * GW];
-    float wa[2 * GW], wb[2 * GW];
-    if (rounds > 0) {
-      load_u32<2 * GW>(op, oa);
-      load_f32<2 * GW>(wp, wa);
-    }
-#pragma unroll 1
-    for (int r = 0; r < rounds; r += 4) {
-      load_u32<2 * GW>(op + (r + 2) * GW, ob);
-      load_f32<2 * GW>(wp + (r + 2) * GW, wb);
-      sum_rounds<S, G, GW>(acc, oa, wa, vb);
-      if (r + 2 >= rounds) break;
-      load_u32<2 * GW>(op + (r + 4) * GW, oa);
-      load_f32<2 * GW>(wp + (r + 4) * GW, wa);
-      sum_rounds<S, G, GW>(acc, ob, wb, vb);
-    }
-  }
-  if constexpr (TANH) {
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const float rk = rk_j[j], bk = bk_j[j];
-      PackT y;
-      if constexpr (S == 1) {
-        y.v[0] = fmaf(2.0f, rcp_approx(1.0f + ex2_approx(fmaf(rk, acc[j][0].x, bk))), -1.0f);
-      } else {
-#pragma unroll
-        for (int p = 0; p < SP; ++p) {
-          const float2 t = __ffma2_rn(make_float2(rk, rk), acc[j][p], make_float2(bk, bk));
-          const float2 d = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(ex2_approx(t.x), ex2_approx(t.y)));
-          const float2 yy = __ffma2_rn(make_float2(2.0f, 2.0f), make_float2(rcp_approx(d.x), rcp_approx(d.y)),
-                                       make_float2(-1.0f, -1.0f));
-          y.v[2 * p] = yy.x;
-          y.v[2 * p + 1] = yy.y;
-        }
-      }
-      if (slot_j[j] != NO_SLOT) *reinterpret_cast<PackT*>(vb + slot_j[j] * RB) = y;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      float a[S];
-#pragma unroll
-      for (int s = 0; s < S; ++s) a[s] = (s & 1) ? acc[j][s / 2].y : acc[j][s / 2].x;
-      finish_step<S, RB>(st[j], a, vb);
-    }
+  for (int c = 0; c < 8; ++c) {
+    const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
+    x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
   }
 }
 
-// non-sum singleton (product / max / min): exact counts in both blocks
-template <int S, int RB>
-__device__ __forceinline__ void run_split_generic(const GroupSplit& gr, const uint32_t* __restrict__ off_s,
-                                                  const float* __restrict__ w_s, const StepT<float>& st, char* vb,
-                                                  uint32_t tlane) {
-  float acc[S];
-  const float neutral = agg_neutral<float>(st.agg);
-#pragma unroll
-  for (int s = 0; s < S; ++s) acc[s] = neutral;
-  for (int e = 0; e < gr.cnt_in[0]; ++e) {
-    float v[S];
-    tmem_ld_cols<S>(tlane + off_s[gr.e_in + e], v);
-    tmem_wait_ld(v);
-    const float w = w_s[gr.e_in + e];
-#pragma unroll
-    for (int s = 0; s < S; ++s) acc[s] = agg_combine<float>(st.agg, acc[s], w * v[s]);
-  }
-  for (int e = 0; e < gr.cnt_h[0]; ++e) {
-    const Pack<float, S> v = *reinterpret_cast<const Pack<float, S>*>(vb + off_s[gr.e_h + e]);
-    const float w = w_s[gr.e_h + e];
-#pragma unroll
-    for (int s = 0; s < S; ++s) acc[s] = agg_combine<float>(st.agg, acc[s], w * v.v[s]);
-  }
-  if (st.count == 0) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) acc[s] = 0.0f;
-  }
-  StepT<float> sum_like = st;
-  sum_like.agg = AGG_SUM;
-  finish_step<S, RB>(sum_like, acc, vb);
+__device__ __forceinline__ float max3_nan(float a, float b, float c) {  // NaN-propagating
+  float d;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
 }
 
-template <int S, int RB, bool EXACT>
-__device__ __forceinline__ void split_sweep(const GroupSplit* gr_s, int n_groups, const uint32_t* off_s,
-                                            const float* w_s, const StepT<float>* st_s, char* vb, uint32_t tlane,
-                                            uint32_t cmask) {
-#pragma unroll 1
-  for (int g = 0; g < n_groups; ++g) {
-    const GroupSplit gr = decode_group(gr_s, g);
-    const StepT<float>* st = st_s + gr.step_begin;
-    if (gr.cls & GRP_GENERIC) {
-      run_split_generic<S, RB>(gr, off_s, w_s, st[0], vb, tlane);
-    } else if (gr.cls & GRP_TANH_SUM) {
-      switch (gr.n) {
-        case 1: run_split_group<S, 1, RB, true, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
-        case 2: run_split_group<S, 2, RB, true, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
-        case 3: run_split_group<S, 3, RB, true, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
-        default: run_split_group<S, 4, RB, true, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
-      }
-    } else {
-      switch (gr.n) {
-        case 1: run_split_group<S, 1, RB, false, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
-        case 2: run_split_group<S, 2, RB, false, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
-        case 3: run_split_group<S, 3, RB, false, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
-        default: run_split_group<S, 4, RB, false, EXACT>(gr, off_s, w_s, st, vb, tlane, cmask); break;
-      }
+// block exponent of a row; returns whether the row takes the exact path (a
+// non-finite input makes the NaN-propagating max non-finite)
+__device__ __forceinline__ bool tc_row_scale(const float (&x)[TC_K], int& ex) {
+  float m = 0.0f;
+#pragma unroll
+  for (int k = 0; k < TC_K; k += 2) m = max3_nan(m, fabsf(x[k]), fabsf(x[k + 1]));
+  const bool exact = !(m < 0x1p62f) || (m != 0.0f && m < 0x1p-62f);
+  ex = (m > 0.0f && !exact) ? float_exponent(m) : 0;
+  return exact;
+}
+
+// digit planes of one row into A row r (exact rows: zero digits).  d0 is left
+// unrounded (r0 * sc, |.| <= 512): the fp16 conversion keeps it to 1/4 and it
+// only enters the 2^-20-weighted class 2
+__device__ __forceinline__ void tc_store_digits(const float (&x)[TC_K], int ex, bool exact, int r, uint8_t* a_half) {
+  const float s20 = exact ? 0.0f : pow2f(7 - ex), i20 = exact ? 0.0f : pow2f(ex - 7);
+  const float s10 = exact ? 0.0f : pow2f(17 - ex), i10 = exact ? 0.0f : pow2f(ex - 17);
+  const float s0 = exact ? 0.0f : pow2f(27 - ex);
+  const float2 M = make_float2(12582912.0f, 12582912.0f), nM = make_float2(-12582912.0f, -12582912.0f);
+  const float2 S20 = make_float2(s20, s20), NI20 = make_float2(-i20, -i20), S10 = make_float2(s10, s10),
+               NI10 = make_float2(-i10, -i10), S0 = make_float2(s0, s0);
+#pragma unroll
+  for (int q = 0; q < TC_K / 8; ++q) {  // 8 inputs = one 16-byte chunk per plane
+    uint32_t w2[4], w1[4], w0[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const float2 xv = make_float2(x[8 * q + 2 * h], x[8 * q + 2 * h + 1]);
+#ifdef TNEAT_DIAG_TC_NOCONV  // diagnostic builds only: no digit arithmetic
+      w2[h] = w1[h] = w0[h] = pack_half2(xv.x, xv.y);
+      continue;
+#endif
+      const float2 d2 = __fadd2_rn(__ffma2_rn(xv, S20, M), nM);
+      const float2 r1 = __ffma2_rn(d2, NI20, xv);
+      const float2 d1 = __fadd2_rn(__ffma2_rn(r1, S10, M), nM);
+      const float2 d0 = __fmul2_rn(__ffma2_rn(d1, NI10, r1), S0);
+      w2[h] = pack_half2(d2.x, d2.y);
+      w1[h] = pack_half2(d1.x, d1.y);
+      w0[h] = pack_half2(d0.x, d0.y);
     }
+    *reinterpret_cast<uint4*>(a_half + tc_offset(r, 8 * q)) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+    *reinterpret_cast<uint4*>(a_half + tc_offset(r, TC_K + 8 * q)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+    *reinterpret_cast<uint4*>(a_half + tc_offset(r, 2 * TC_K + 8 * q)) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
   }
 }
 
-template <int S>
-__global__ void __launch_bounds__(SPLIT_NT, TNEAT_SPLIT_WARPS / 4)
-fwd_split_kernel(const uint8_t* __restrict__ prog, ProgLayout L, const int32_t* __restrict__ genome_ids,
-                 const float* __restrict__ in, int64_t in_gstride, int B, int I, int O, int runs, int tpc,
-                 uint32_t tcols, float* __restrict__ out, int64_t out_gstride) {
-  constexpr int TT = SPLIT_NT * S;
-  constexpr int RB = (TT + S) * 4;  // bytes of one hidden value slot row (padded by S)
-  using PackT = Pack<float, S>;
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t tmem_base;
-  __shared__ uint16_t oslot[8];
-  const int64_t task = blockIdx.x / runs;
-  const int run = (int)(blockIdx.x - task * runs);
-  const int64_t gi = genome_ids ? (int64_t)__ldg(genome_ids + task) : task;
-  const uint8_t* gp = prog + gi * L.stride;
-  const ProgHeader hdr = *reinterpret_cast<const ProgHeader*>(gp);
-  const int n_steps = hdr.n_steps, n_edges = hdr.n_edges, n_groups = hdr.n_groups;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const float* gin = in + gi * in_gstride;
-  const bool vec_in = (I & 3) == 0 && (((uintptr_t)gin) & 15) == 0;
-  if (tid == 0 && vec_in) {
-    const int t0 = run * tpc * TT;
-    if (t0 < B) prefetch_l2(gin + (int64_t)t0 * I, (uint32_t)(min(TT, B - t0) * I * 4));
-  }
-  // shared memory: groups | steps | u32 offsets | weights | hidden values [slot][TT + S]
-  GroupSplit* gr_s = reinterpret_cast<GroupSplit*>(smem);
-  const int64_t off_st = (int64_t)n_groups * sizeof(GroupSplit);
-  StepT<float>* st_s = reinterpret_cast<StepT<float>*>(smem + off_st);
-  const int64_t off_src = off_st + (int64_t)n_steps * sizeof(StepT<float>);
-  uint32_t* off_s = reinterpret_cast<uint32_t*>(smem + off_src);
-  const int64_t off_w = off_src + align_up(4ll * n_edges, 16);
-  float* w_s = reinterpret_cast<float*>(smem + off_w);
-  float* vals = reinterpret_cast<float*>(smem + align_up(off_w + 4ll * n_edges, 16));
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+struct TcShared {
+  uint64_t gbar[2];                 // genome block staged in buffer b
+  uint64_t tma_bar[TC_MAX_WG];      // input tile of warpgroup w
+  uint64_t mma_bar[TC_MAX_WG];      // MMAs of warpgroup w done
+  uint32_t tmem_base;
+  uint32_t tmem_mask;               // TMEM column slots in use
+  uint32_t slot_col[TC_MAX_WG];     // column offset of warpgroup w's slot
+  int32_t hdr[2][4];                // n_steps, n_edges, n_groups, genome of buffer b
+  uint16_t oslot[2][8];
+};
+
+__global__ void __launch_bounds__(TC_NT* TC_MAX_WG, 1)
+fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __restrict__ prog, ProgLayout L,
+              const int32_t* __restrict__ genome_ids, int64_t P, const float* __restrict__ in, int64_t in_gstride,
+              int B, int I, int O, int nwg, uint32_t wg_bytes, uint32_t gbuf_bytes, int nbuf, int nb_max,
+              float* __restrict__ out,
+              int64_t out_gstride) {
+  // no static shared memory: the dynamic area starts the CTA's shared window,
+  // 1024-aligned for the swizzled TMA tiles; the control block is at its end
+  extern __shared__ __align__(1024) uint8_t smem[];
+  TcShared& sh = *reinterpret_cast<TcShared*>(smem + (uint32_t)nwg * wg_bytes + (uint32_t)nbuf * gbuf_bytes);
+  const int tid = threadIdx.x, warp = tid >> 5, wg = tid >> 7, wt = tid & (TC_NT - 1);
+  const int bar_id = 1 + wg;
+  uint8_t* const wg_area = smem + (uint32_t)wg * wg_bytes;
+  uint8_t* const gbuf0 = smem + (uint32_t)nwg * wg_bytes;
+  const uint32_t slot_cols = 4u * (uint32_t)nb_max;
+  const uint32_t n_slots = 512u / slot_cols;
+  const int tiles = (B + TC_TT - 1) / TC_TT;
+
+  auto issue_stage = [&](int64_t task, int buf) {  // one thread: header + block of genome `task`
+    const int64_t gi = genome_ids ? (int64_t)__ldg(genome_ids + task) : task;
+    const uint8_t* gp = prog + gi * L.stride;
+    const ProgHeader hdr = *reinterpret_cast<const ProgHeader*>(gp);
+    const int ns = hdr.mode == MODE_TC ? hdr.n_steps : 0, ng = hdr.mode == MODE_TC ? hdr.n_groups : 0;
+    const int ne = hdr.mode == MODE_TC ? hdr.n_edges : 0;
+    sh.hdr[buf][0] = ns; sh.hdr[buf][1] = ne; sh.hdr[buf][2] = ng; sh.hdr[buf][3] = (int)gi;
+    const uint16_t* os = reinterpret_cast<const uint16_t*>(gp + L.off_out);
+    for (int o = 0; o < 8; ++o) sh.oslot[buf][o] = (o < O && hdr.mode == MODE_TC) ? __ldg(os + o) : NO_SLOT;
+    const TcBlock tb = tc_block(ns, ng, ne);
+    const uint32_t bar = smem_u32(&sh.gbar[buf]);
+    mbar_expect_tx(bar, tb.bytes);
+    if (tb.bytes) bulk_g2s(smem_u32(gbuf0 + (uint32_t)buf * gbuf_bytes), gp + L.off_tc, tb.bytes, bar);
+  };
 
   if (warp == 0) {
-    tmem_alloc(smem_u32(&tmem_base), tcols);
+    tmem_alloc(smem_u32(&sh.tmem_base), 512);
     tmem_relinquish();
   }
-  {
-    auto copy16 = [&](void* dst, const void* src, int64_t bytes) {
-      const int n16 = (int)(bytes / 16);
-      for (int i = tid; i < n16; i += SPLIT_NT)
-        reinterpret_cast<int4*>(dst)[i] = __ldg(reinterpret_cast<const int4*>(src) + i);
-    };
-    copy16(gr_s, gp + L.off_groups, off_st);
-    copy16(st_s, gp + L.off_steps, (int64_t)n_steps * sizeof(StepT<float>));
-    copy16(w_s, gp + L.off_w, 4ll * n_edges);
-    const uint32_t* gs = reinterpret_cast<const uint32_t*>(gp + L.off_src);  // raw u16 pairs
-    for (int i = tid; i < n_edges / 2; i += SPLIT_NT) {
-      const uint32_t pr = __ldg(gs + i);
-      reinterpret_cast<uint2*>(off_s)[i] = make_uint2(pr & 0xFFFFu, pr >> 16);
+  if (tid == 0) {
+    mbar_init(smem_u32(&sh.gbar[0]), 1);
+    mbar_init(smem_u32(&sh.gbar[1]), 1);
+    for (int w = 0; w < TC_MAX_WG; ++w) {
+      mbar_init(smem_u32(&sh.tma_bar[w]), 1);
+      mbar_init(smem_u32(&sh.mma_bar[w]), 1);
     }
-  }
-  const uint16_t* os = reinterpret_cast<const uint16_t*>(gp + L.off_out);
-  if (tid < 8) oslot[tid] = tid < O ? __ldg(os + tid) : NO_SLOT;
-  if (hdr.n_slots > 0)
-    for (int i = tid; i < TT + S; i += SPLIT_NT) vals[(int64_t)(hdr.n_slots - 1) * (RB / 4) + i] = 0.0f;
-  __syncthreads();
-  // scale the raw sources: input blocks -> TMEM column offset k*S, hidden blocks -> byte offset slot*RB
-  for (int g = tid; g < n_groups; g += SPLIT_NT) {
-    const GroupSplit gr = gr_s[g];
-    const int gw = group_width(gr.n);
-    for (int e = gr.e_in; e < gr.e_in + gw * gr.rounds_in; ++e) off_s[e] *= (uint32_t)S;
-    for (int e = gr.e_h; e < gr.e_h + gw * gr.rounds_h; ++e) off_s[e] *= (uint32_t)RB;
+    sh.tmem_mask = 0u;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (blockIdx.x < P) issue_stage(blockIdx.x, 0);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tlane = tmem_base + ((uint32_t)(warp * 32) << 16);
-  char* vb = reinterpret_cast<char*>(vals) + tid * S * 4;
-  bool fast_out = O == 8;
+  const uint32_t tmem = sh.tmem_base;
+  const uint32_t bar_tma = smem_u32(&sh.tma_bar[wg]), bar_mma = smem_u32(&sh.mma_bar[wg]);
+  uint8_t* const in_area = wg_area + wg_bytes - TC_IN_BYTES;  // input tile: end of the area
+  const uint32_t in_addr = smem_u32(in_area);
+  char* const vb = reinterpret_cast<char*>(wg_area) + wt * 8;
+  const uint32_t a_addr = smem_u32(wg_area);
+  uint32_t tphase = 0, mphase = 0, gphase[2] = {0u, 0u};
+
+  int k = 0;
+  for (int64_t task = blockIdx.x; task < P; task += gridDim.x, ++k) {
+    // two buffers: the next genome's block is in flight during this one; one
+    // buffer (when a second would cost a warpgroup): staged after the barrier
+    const int buf = nbuf == 2 ? (k & 1) : 0;
+    mbar_wait(smem_u32(&sh.gbar[buf]), gphase[buf]);
+    gphase[buf] ^= 1u;
+    if (nbuf == 2 && tid == 0 && task + gridDim.x < P) issue_stage(task + gridDim.x, buf ^ 1);
+    const int n_steps = sh.hdr[buf][0], n_edges = sh.hdr[buf][1], n_groups = sh.hdr[buf][2];
+    const int64_t gi = sh.hdr[buf][3];
+    const int nb = tc_rows(n_steps);
+    const TcBlock tb = tc_block(n_steps, n_groups, n_edges);
+    uint8_t* const gb = gbuf0 + (uint32_t)buf * gbuf_bytes;
+    const GroupRec* gr_s = reinterpret_cast<const GroupRec*>(gb + tb.gr);
+    const StepT<float>* st_s = reinterpret_cast<const StepT<float>*>(gb + tb.st);
+    const uint32_t* src_s = reinterpret_cast<const uint32_t*>(gb + tb.src);
+    const float* w_s = reinterpret_cast<const float*>(gb + tb.w);
+    const float* cf_s = reinterpret_cast<const float*>(gb + tb.cf);
+    const uint32_t b_addr = smem_u32(gb + tb.b);
+    const uint16_t* oslot = sh.oslot[buf];
+    bool fast_out = O == 8 && n_steps > 0;
 #pragma unroll
-  for (int o = 0; o < 8; ++o) fast_out = fast_out && oslot[o] != NO_SLOT;
-  float* go = out + gi * out_gstride;
-  const int tile_end = min((run + 1) * tpc, (B + TT - 1) / TT);
-  for (int tile = run * tpc; tile < tile_end; ++tile) {
-    const int t0 = tile * TT;
-    if (tid == 0 && vec_in && tile + 1 < tile_end) {
-      const int t1 = t0 + TT;
-      prefetch_l2(gin + (int64_t)t1 * I, (uint32_t)(min(TT, B - t1) * I * 4));
+    for (int o = 0; o < 8; ++o) fast_out = fast_out && oslot[o] != NO_SLOT;
+    const uint8_t* gp = prog + gi * L.stride;
+    const float* gin = in + gi * in_gstride;
+    float* go = out + gi * out_gstride;
+    const int zc = in_gstride ? (int)gi : 0;  // input tensor map: (I, B, genomes)
+    const bool pf_l2 = ((uintptr_t)gin & 15) == 0;
+    const uint16_t* in_start = reinterpret_cast<const uint16_t*>(gp + L.off_in);
+    const uint16_t* isrc = reinterpret_cast<const uint16_t*>(gp + L.off_isrc);
+    const float* iw = reinterpret_cast<const float*>(gp + L.off_iw);
+
+    if (n_steps > 0 && wt == 0 && wg < tiles) {  // this warpgroup's first tile
+      mbar_expect_tx(bar_tma, TC_IN_BYTES);
+      tma_load_3d(in_addr, &tmap_in, 0, wg * TC_TT, zc, bar_tma);
     }
-    const int s0 = t0 + tid * S;
-    // own input rows -> TMEM lane (column k*S + s), eight columns per store
-    float2 nf = make_float2(0.0f, 0.0f);  // x * 0 sums: NaN iff some input is not finite
-    for (int k0 = 0; k0 < I; k0 += 8 / S) {
-      float c[8];
+    for (int tile = wg; tile < tiles && n_steps > 0; tile += nwg) {
+      const int s0 = tile * TC_TT + wt, s1 = s0 + TC_NT;  // this thread's samples
+      const int next = tile + nwg;
+      // ---- 1-2: input rows -> block scales -> digit planes (A rows wt of both halves)
+      mbar_wait_sleep(bar_tma, tphase);
+      tphase ^= 1u;
+      if (wt == 0 && next < tiles && pf_l2)  // next tile: HBM -> L2 while this one computes
+        prefetch_l2(gin + (int64_t)next * TC_TT * I, (uint32_t)(min(TC_TT, B - next * TC_TT) * I * 4));
+      // the input tile sits at the end of the area: A half 0 ([0, 24K)) only
+      // overlaps input rows of half 0, so each half is read (into registers),
+      // then its digits are written
+      int ex0, ex1;
+      bool exact0, exact1;
+      {
+        float x[TC_K];
+        tc_load_row(in_area + wt * 128, wt, x);
+        exact0 = tc_row_scale(x, ex0);
+        named_barrier_sync(bar_id, TC_NT);
+        tc_store_digits(x, ex0, exact0, wt, wg_area);
+      }
+      {
+        float x[TC_K];
+        tc_load_row(in_area + (TC_NT + wt) * 128, wt, x);
+        exact1 = tc_row_scale(x, ex1);
+        named_barrier_sync(bar_id, TC_NT);
+        tc_store_digits(x, ex1, exact1, wt, wg_area + TC_A_HALF);
+      }
+      fence_proxy_async_smem();
+      // ---- 3: a TMEM column slot, MMAs (one thread) -------------------------------------
+      if (wt == 0) {
+        uint32_t slot = (uint32_t)wg;
+        if (n_slots < (uint32_t)nwg) {  // fewer slots than warpgroups: take a free one
+          for (;;) {
+            const uint32_t m = *reinterpret_cast<volatile uint32_t*>(&sh.tmem_mask);
+            slot = __ffs(~m) - 1;
+            if (slot < n_slots && atomicCAS(&sh.tmem_mask, m, m | (1u << slot)) == m) break;
+            __nanosleep(32);
+          }
+        }
+        sh.slot_col[wg] = slot * slot_cols;
+      }
+      tc_fence_before();
+      named_barrier_sync(bar_id, TC_NT);  // A complete, column slot taken
+      tc_fence_after();
+      const uint32_t dcol = tmem + sh.slot_col[wg];
+      if (wt < 32)
+        tc_issue_mmas(__shfl_sync(0xffffffffu, a_addr, 0), __shfl_sync(0xffffffffu, b_addr, 0),
+                      __shfl_sync(0xffffffffu, dcol, 0), __shfl_sync(0xffffffffu, nb, 0), bar_mma);
+      // ---- 4: TMEM -> input partials in the step slots ------------------------------------
+      mbar_wait_sleep(bar_mma, mphase);
+      mphase ^= 1u;
+      tc_fence_after();
+      {
+        // warp-uniform TMEM address (uniform registers for tcgen05.ld)
+        const uint32_t t_lane = __shfl_sync(0xffffffffu, dcol + ((uint32_t)((warp & 3) * 32) << 16), 0);
+        // partial / cf = T * 2^(ex - 12): the column factor cf lives in the step
+        // (response and hidden weights, transform.cu)
+        const float2 rf0 = make_float2(pow2f(ex0 - 12), pow2f(ex0 - 12));
+        const float2 rf1 = make_float2(pow2f(ex1 - 12), pow2f(ex1 - 12));
+        const float2 k1024 = make_float2(1024.0f, 1024.0f);
+#pragma unroll 1
+#ifdef TNEAT_DIAG_TC_NOEPI  // diagnostic builds only: no TMEM -> slot epilogue
+        for (int c = 0; c < 0; c += 8) {
+#else
+        for (int c = 0; c < nb; c += 8) {
+#endif
+          uint32_t a4[8], a3[8], b4[8], b3[8];
+          TMEM_LD8(t_lane + (uint32_t)c, a4);
+          TMEM_LD8(t_lane + (uint32_t)(nb + c), a3);
+          TMEM_LD8(t_lane + (uint32_t)(2 * nb + c), b4);
+          TMEM_LD8(t_lane + (uint32_t)(3 * nb + c), b3);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        const bool ok = s0 + s < B;
-        const float* row = gin + (int64_t)(ok ? s0 + s : 0) * I + k0;
-#pragma unroll
-        for (int kk = 0; kk < 8 / S; ++kk) c[kk * S + s] = 0.0f;
-        if (ok) {
-          if (vec_in) {
-#pragma unroll
-            for (int h = 0; h < 8 / S; h += 4) {
-              if (k0 + h < I) {
-                const float4 x = __ldg(reinterpret_cast<const float4*>(row + h));
-                c[(h + 0) * S + s] = x.x; c[(h + 1) * S + s] = x.y; c[(h + 2) * S + s] = x.z; c[(h + 3) * S + s] = x.w;
-              }
+          for (int i = 0; i < 8; i += 2) {  // steps c+i, c+i+1: packed over adjacent columns
+            const float2 p0 =
+                __fmul2_rn(__ffma2_rn(make_float2(__uint_as_float(a4[i]), __uint_as_float(a4[i + 1])), k1024,
+                                      make_float2(__uint_as_float(a3[i]), __uint_as_float(a3[i + 1]))),
+                           rf0);
+            const float2 p1 =
+                __fmul2_rn(__ffma2_rn(make_float2(__uint_as_float(b4[i]), __uint_as_float(b4[i + 1])), k1024,
+                                      make_float2(__uint_as_float(b3[i]), __uint_as_float(b3[i + 1]))),
+                           rf1);
+            *reinterpret_cast<float2*>(vb + (uint32_t)(c + i) * TC_RB) = make_float2(p0.x, p1.x);
+            *reinterpret_cast<float2*>(vb + (uint32_t)(c + i + 1) * TC_RB) = make_float2(p0.y, p1.y);
+          }
+        }
+        tc_fence_before();
+        named_barrier_sync(bar_id, TC_NT);  // every warp has read its lanes: release the slot
+        if (wt == 0 && n_slots < (uint32_t)nwg) atomicAnd(&sh.tmem_mask, ~(1u << (sh.slot_col[wg] / slot_cols)));
+        *reinterpret_cast<float2*>(vb + (uint32_t)n_steps * TC_RB) = make_float2(0.0f, 0.0f);  // zero slot
+        if (exact0 || exact1) {  // exact fp32 partials (program order of each step's input edges)
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            const int s = h ? s1 : s0;
+            if (!(h ? exact1 : exact0) || s >= B) continue;
+            const float* xr = gin + (int64_t)s * I;
+            for (int kk = 0; kk < n_steps; ++kk) {
+              float p = 0.0f;
+              for (int e = __ldg(in_start + kk); e < __ldg(in_start + kk + 1); ++e)
+                p = fmaf(__ldg(iw + e), __ldg(xr + __ldg(isrc + e)), p);
+              reinterpret_cast<float*>(vb + (uint32_t)kk * TC_RB)[h] = p * cf_s[kk];  // cf_s: 1 / cf
             }
-          } else {
-#pragma unroll
-            for (int kk = 0; kk < 8 / S; ++kk)
-              if (k0 + kk < I) c[kk * S + s] = __ldg(row + kk);
           }
         }
       }
-#pragma unroll
-      for (int q = 0; q < 8; q += 2) nf = __ffma2_rn(make_float2(c[q], c[q + 1]), make_float2(0.0f, 0.0f), nf);
-      tmem_st8(tlane + (uint32_t)(k0 * S), c);
-    }
-    tmem_wait_st();
-    const bool exact = __any_sync(0xffffffffu, nf.x != nf.x || nf.y != nf.y);
-    if (exact) split_sweep<S, RB, true>(gr_s, n_groups, off_s, w_s, st_s, vb, tlane, tcols - 1);
-    else split_sweep<S, RB, false>(gr_s, n_groups, off_s, w_s, st_s, vb, tlane, tcols - 1);
-
-    if (fast_out) {
-      PackT v[8];
-#pragma unroll
-      for (int o = 0; o < 8; ++o) v[o] = *reinterpret_cast<const PackT*>(vb + (uint32_t)oslot[o] * RB);
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        if (s0 + j >= B) break;
-        float4* row = reinterpret_cast<float4*>(go + (int64_t)(s0 + j) * 8);
-        row[0] = make_float4(v[0].v[j], v[1].v[j], v[2].v[j], v[3].v[j]);
-        row[1] = make_float4(v[4].v[j], v[5].v[j], v[6].v[j], v[7].v[j]);
+#ifdef TNEAT_DIAG_TC_EARLYTMA  // diagnostic builds only (wrong results): next tile's TMA before the sweep
+      if (wt == 0 && next < tiles) {
+        mbar_expect_tx(bar_tma, TC_IN_BYTES);
+        tma_load_3d(in_addr, &tmap_in, 0, next * TC_TT, zc, bar_tma);
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        if (s0 + j >= B) break;
-        float* row = go + (int64_t)(s0 + j) * O;
-        for (int o = 0; o < O; ++o) {
-          const uint16_t sl = __ldg(os + o);
-          row[o] = sl != NO_SLOT ? *reinterpret_cast<const float*>(vb + sl * RB + j * 4) : NAN;
+#endif
+      // ---- 5: hidden-edge sweep ---------------------------------------------------------
+      {
+        Words wd;
+        if (n_groups > 0) load_words(wd, src_s, w_s, (int)reinterpret_cast<const uint4*>(gr_s)[0].z);
+#ifdef TNEAT_DIAG_TC_NOSWEEP  // diagnostic builds only: no hidden-edge sweep
+        const int n_groups_run = 0;
+#else
+        const int n_groups_run = n_groups;
+#endif
+#pragma unroll 1
+        for (int g = 0; g < n_groups_run; ++g) {
+          // the record and the next group's first entry (its words are loaded
+          // at the end of this group; past the last group: the step table)
+          const uint4 raw = reinterpret_cast<const uint4*>(gr_s)[g];
+          const int next_e = (int)reinterpret_cast<const uint4*>(gr_s)[g + 1].z;
+          run_group_tc(raw, src_s, w_s, st_s, vb, wd, g + 1 < n_groups ? next_e : 0);
         }
       }
+      // ---- outputs (P, B, O) ------------------------------------------------------------
+      if (fast_out) {
+        float2 v[8];
+#pragma unroll
+        for (int o = 0; o < 8; ++o) v[o] = *reinterpret_cast<const float2*>(vb + (uint32_t)oslot[o] * TC_RB);
+        if (s0 < B) {
+          float4* row = reinterpret_cast<float4*>(go + (int64_t)s0 * 8);
+          row[0] = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
+          row[1] = make_float4(v[4].x, v[5].x, v[6].x, v[7].x);
+        }
+        if (s1 < B) {
+          float4* row = reinterpret_cast<float4*>(go + (int64_t)s1 * 8);
+          row[0] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
+          row[1] = make_float4(v[4].y, v[5].y, v[6].y, v[7].y);
+        }
+      } else {
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          const int s = h ? s1 : s0;
+          if (s >= B) continue;
+          float* row = go + (int64_t)s * O;
+          const uint16_t* os = reinterpret_cast<const uint16_t*>(gp + L.off_out);
+          for (int o = 0; o < O; ++o) {
+            const uint16_t sl = __ldg(os + o);
+            row[o] = sl != NO_SLOT ? reinterpret_cast<const float*>(vb + (uint32_t)sl * TC_RB)[h] : NAN;
+          }
+        }
+      }
+      named_barrier_sync(bar_id, TC_NT);  // slots dead: the next tile's inputs may land
+#ifndef TNEAT_DIAG_TC_EARLYTMA
+      if (wt == 0 && next < tiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar_tma, TC_IN_BYTES);
+        tma_load_3d(in_addr, &tmap_in, 0, next * TC_TT, zc, bar_tma);
+      }
+#endif
     }
+    __syncthreads();  // every warpgroup is done with buffer `buf` before it is restaged
+    if (nbuf == 1 && tid == 0 && task + gridDim.x < P) issue_stage(task + gridDim.x, 0);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, tcols);
+    tmem_dealloc(tmem, 512);
   }
 }
 
-// ---------------------------------------------------------------------------
-// warp-per-(genome, input chunk) kernel for small batches
 // ---------------------------------------------------------------------------
 
 template <typename T> __device__ __forceinline__ T warp_allreduce(int agg, T v) {
@@ -1334,31 +1440,48 @@ int launch_tile(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, co
   return 0;
 }
 
-// split programs: maxdims_host = (hidden slots incl. zero slot, steps, edge entries)
-// maxima over the launched genomes
-int launch_split(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, const float* in,
-                 int64_t in_gstride, int64_t P, int B, int I, int O, const int32_t* maxdims_host, float* out,
-                 int64_t out_gstride, int tpc, cudaStream_t st) {
-  constexpr int S = 2, TT = SPLIT_NT * S, RB = (TT + S) * 4;
-  if (I * S > 512) return -8;
-  const int tiles = (B + TT - 1) / TT;
-  tpc = max(1, min(tpc, tiles));
-  const int runs = (tiles + tpc - 1) / tpc;
-  const int64_t grid = P * runs;
-  if (grid > 0x7FFFFFFFll) return -5;
-  const int64_t slots = maxdims_host[0] > 1 ? maxdims_host[0] : 1, ms = maxdims_host[1], me = maxdims_host[2];
-  uint32_t tcols = 32;
-  while (tcols < (uint32_t)(I * S)) tcols <<= 1;
-  int64_t smem = align_up(32 * ms + 16 * ms, 16) + align_up(4 * me, 16) + align_up(4 * me, 16) + slots * RB;
-  // no more resident CTAs per SM than the TMEM columns allow (an allocation
-  // that does not fit would spin until another CTA on the SM exits)
-  const int tmem_ctas = 512 / (int)tcols;
-  const int64_t smem_floor = (228ll * 1024) / (tmem_ctas + 1) - 1024 + 64;
-  if (smem < smem_floor) smem = smem_floor;
-  if (smem > 227 * 1024) return -6;
-  cudaFuncSetAttribute(fwd_split_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fwd_split_kernel<S><<<(unsigned)grid, SPLIT_NT, smem, st>>>(prog, L, ids, in, in_gstride, B, I, O, runs, tpc,
-                                                               tcols, out, out_gstride);
+// TC programs: maxdims_host = (slots, steps, edge entries) maxima over the
+// launched genomes (all MODE_TC).  Persistent grid: one CTA per SM (or fewer
+// for small launches) with as many warpgroups as shared memory allows.
+int launch_tc(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, const float* in, int64_t in_gstride,
+              int64_t P, int B, int I, int O, const int32_t* maxdims_host, float* out, int64_t out_gstride,
+              int max_wg, cudaStream_t st) {
+  if (I > TC_K || (I & 3) || (((uintptr_t)in) & 15)) return -8;
+  const int ms = max(maxdims_host[1], 1), me = maxdims_host[2];
+  const int nb = tc_rows(ms);
+  if (4 * nb > 512) return -8;
+  const uint32_t wg_bytes = tc_wg_bytes(nb);
+  const uint32_t gbuf = (uint32_t)align_up(tc_block(ms, ms, me).bytes + 64, 128);  // + look-ahead slack
+  const int64_t budget = 227 * 1024, ctl = (int64_t)align_up(sizeof(TcShared), 16);
+  auto fit = [&](int nbuf) {
+    int w = max_wg > 0 ? min(max_wg, TC_MAX_WG) : TC_MAX_WG;
+    while (w > 1 && ctl + nbuf * (int64_t)gbuf + (int64_t)w * wg_bytes > budget) --w;
+    return w;
+  };
+  // double-buffered genome blocks unless a single buffer buys another warpgroup
+  const int nbuf = fit(1) > fit(2) ? 1 : 2;
+  const int nwg = fit(nbuf);
+  const int64_t smem = ctl + nbuf * (int64_t)gbuf + (int64_t)nwg * wg_bytes;
+  if (smem > budget) return -6;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = P < sms ? P : sms;
+  const PFN_cuTensorMapEncodeTiled_v12000 encode = tmap_encoder();
+  if (!encode) return -9;
+  // inputs as an (I, B, genomes) fp32 tensor; boxes of 32 inputs x 256 rows
+  // (zero fill past I and B), 128-byte swizzle (conflict-free row reads)
+  CUtensorMap tmap;
+  const cuuint64_t dims[3] = {(cuuint64_t)I, (cuuint64_t)B, in_gstride ? (cuuint64_t)1 << 30 : 1};
+  const cuuint64_t strides[2] = {(cuuint64_t)I * 4, (cuuint64_t)(in_gstride ? in_gstride : (int64_t)B * I) * 4};
+  const cuuint32_t box[3] = {TC_K, TC_TT, 1}, estr[3] = {1, 1, 1};
+  if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -9;
+  cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  fwd_tc_kernel<<<(unsigned)grid, TC_NT * nwg, smem, st>>>(tmap, prog, L, ids, P, in, in_gstride, B, I, O, nwg,
+                                                           wg_bytes, gbuf, nbuf, nb, out, out_gstride);
   TNEAT_CHECK_LAUNCH();
   return 0;
 }
@@ -1384,16 +1507,18 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
   const int64_t ogs = (int64_t)B * O;
   // variant (low 4 bits): 0 = auto, 1 = tile S=1 (128 thr), 2 = tile S=2 (128 thr),
   // 3 = tile S=1 (64 thr), 4 = tile S=4 (64 thr), 5 = tile S=2 (64 thr), 6 = tile S=4 (32 thr),
-  // 8 = warp kernel, 10 = split kernel (split programs: the only one, and auto);
-  // bits 8..15 = tiles per CTA (0 = default 4)
+  // 8 = warp kernel, 11 = tensor-core kernel (FMT_TC programs whose header
+  // mode is MODE_TC; the other genomes of an FMT_TC population are standard
+  // programs for the variants above); bits 8..15 = tiles per CTA (0 = default
+  // 4; tensor-core kernel: maximum warpgroups per CTA, 0 = as many as fit)
   int tpc = (variant >> 8) & 0xFF;
-  if (tpc == 0) tpc = 4;
   variant &= 0xF;
-  if (precision & FMT_SPLIT) {  // split programs run on the split kernel only
-    if (variant != 0 && variant != 10) return -7;
-    return launch_split(pg, L, genome_ids, (const float*)inputs, input_genome_stride, P, B, I, O, maxdims_host,
-                        (float*)outputs, ogs, tpc, st);
+  if (variant == 11) {
+    if (!(precision & FMT_TC)) return -7;
+    return launch_tc(pg, L, genome_ids, (const float*)inputs, input_genome_stride, P, B, I, O, maxdims_host,
+                     (float*)outputs, ogs, tpc & 0xF, st);
   }
+  if (tpc == 0) tpc = 4;
   if (variant == 0) variant = B >= 192 ? 5 : (B >= 96 ? 3 : 8);
   if (variant == 8) {
     if (genome_ids) return -7;
@@ -1432,12 +1557,12 @@ int an_forward_fitness(const void* program, int64_t program_stride, int N, int C
   if (P < 0 || B < 1 || I < 1 || O != 1 || !maxdims_host || (kind != 1 && kind != 2)) return -1;
   if (kind == 1 && B != 4) return -1;
   if (kind == 2 && !targets) return -2;
-  if (precision & FMT_SPLIT) return -7;
+  if (precision & FMT_TC) return -7;  // standard programs only
   if (P == 0) return 0;
   const ProgLayout L = prog_layout(N, C, O, precision);
   if (L.stride != program_stride) return -3;
   cudaStream_t st = (cudaStream_t)stream;
-  if (precision)
+  if (precision & FMT_F64)
     return launch_warp<double>((const uint8_t*)program, L, P, (const double*)inputs, input_genome_stride, B, I,
                                O, maxdims_host, nullptr, 0, kind, targets, fitness, st);
   return launch_warp<float>((const uint8_t*)program, L, P, (const float*)inputs, input_genome_stride, B, I, O,
@@ -1450,7 +1575,7 @@ int an_cartpole(const void* program, int64_t program_stride, int N, int C, int p
                 const int32_t* maxdims_host, int64_t P, const double* start, int max_steps, double* fitness,
                 void* stream) {
   if (P < 0 || !maxdims_host || max_steps < 0) return -1;
-  if (precision & FMT_SPLIT) return -7;
+  if (precision & FMT_TC) return -7;  // standard programs only
   if (P == 0) return 0;
   const ProgLayout L = prog_layout(N, C, 1, precision);
   if (L.stride != program_stride) return -3;

@@ -18,11 +18,9 @@
 // tanh -> squared error -> running sum) of tile t-1 while the tensor core
 // works on tile t.  Y is never written to memory.
 
-#include <cuda.h>          // CUtensorMap (types only: no link against libcuda)
-#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled, resolved via cudaGetDriverEntryPoint
-
 #include "common.cuh"
 #include "tc.cuh"
+#include "tmap.cuh"
 
 namespace tneat {
 
@@ -209,13 +207,8 @@ int an_substrate_fitness(const float* W, int64_t P, const float* X, const float*
   if (((uintptr_t)W | (uintptr_t)X) & 15) return -2;
   // TMA descriptors: W as a (P*64, 64) and X as an (S, 64) row-major fp32 matrix,
   // boxes of one 4-float K chunk x all tile rows
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q) !=
-            cudaSuccess || q != cudaDriverEntryPointSuccess || !encode)
-      return -9;
-  }
+  const PFN_cuTensorMapEncodeTiled_v12000 encode = tmap_encoder();
+  if (!encode) return -9;
   CUtensorMap tw, tx;
   const cuuint32_t estr[2] = {1, 1};
   {

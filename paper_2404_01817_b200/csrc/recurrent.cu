@@ -165,7 +165,7 @@ int an_rollout(const void* program, int64_t program_stride, int N, int C, int pr
                int D, int steps, int sweeps, double* fitness, void* stream) {
   if (P < 0 || !maxdims_host || D < 1 || steps < 0 || sweeps < 1 || I < 1 || O < 1) return -1;
   if (P == 0) return 0;
-  if (precision & FMT_SPLIT) return -7;
+  if (precision & FMT_TC) return -7;  // standard programs only
   const ProgLayout L = prog_layout(N, C, O, precision);
   if (L.stride != program_stride) return -3;
   const int slots = max(maxdims_host[0], I);

@@ -15,6 +15,8 @@
 // grouped steps with per-step edge lists and liveness-recycled value slots.
 
 #include "common.cuh"
+#include "digits.cuh"
+#include <cuda_fp16.h>
 
 namespace tneat {
 
@@ -95,8 +97,7 @@ struct WarpSmem {
   uint16_t* slot_of;  // [N]
   uint16_t* step_row; // [N]
   uint16_t* grp_of;   // [N]
-  GroupRec* grp;      // [N]      (standard programs)
-  GroupSplit* grps;   // [N]      (split programs; same memory as grp)
+  GroupRec* grp;      // [N]
   uint8_t* flags;     // [N]
   uint8_t* needed;    // [N]
   uint8_t* used;      // [N]
@@ -111,7 +112,7 @@ __host__ __device__ inline int next_pow2(int x) {
 }
 
 template <bool kCarve, typename KT>
-__host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, bool split, WarpSmem<KT>* s) {
+__host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, WarpSmem<KT>* s) {
   using E = typename KT::E;
   using G = typename KT::G;
   const int Npad = next_pow2(N), Cpad = next_pow2(C);
@@ -128,7 +129,7 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, bool
   // the arrays that are first written after Kahn (gkey, grp, last_grp,
   // step_row, grp_of)
   const int64_t a_union = take(0, 16);
-  const int64_t a_gkey = take((int64_t)sizeof(G) * Npad, 8), a_grp = take((split ? 32ll : 16ll) * N, 16);
+  const int64_t a_gkey = take((int64_t)sizeof(G) * Npad, 8), a_grp = take(16ll * N, 16);
   const int64_t a_last = take(4ll * (N + 1), 4);  // also the level starts of the level-synchronous Kahn
   const int64_t a_srow = take(2ll * N, 2), a_grpof = take(2ll * N, 2);
   const int64_t a_ekey2 = a_union;
@@ -153,7 +154,6 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, bool
     s->lvl = (int32_t*)(base + a_lvl);
     s->last_grp = (int32_t*)(base + a_last);
     s->grp = (GroupRec*)(base + a_grp);
-    s->grps = (GroupSplit*)(base + a_grp);
     s->succ = (typename KT::Succ*)(base + a_succ);
     s->order = (uint16_t*)(base + a_order);
     s->slot_of = (uint16_t*)(base + a_slot);
@@ -168,9 +168,9 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, bool
   return align_up(o, 16);
 }
 
-__host__ inline int64_t warp_smem_bytes(int N, int C, bool split) {
-  if (small_keys(N, C)) return layout_warp<false, KeyTraits<true>>(nullptr, N, C, split, nullptr);
-  return layout_warp<false, KeyTraits<false>>(nullptr, N, C, split, nullptr);
+__host__ inline int64_t warp_smem_bytes(int N, int C) {
+  if (small_keys(N, C)) return layout_warp<false, KeyTraits<true>>(nullptr, N, C, nullptr);
+  return layout_warp<false, KeyTraits<false>>(nullptr, N, C, nullptr);
 }
 
 // ascending bitonic sort of n (power of two, >= 32) values, one warp
@@ -271,7 +271,7 @@ __device__ inline int warp_first_set(const uint32_t* words, int nw) {
 
 template <typename T, bool SMALL>
 __global__ void transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
-                                 int64_t P, int N, int C, int I, int O, int mode, int prune, bool split,
+                                 int64_t P, int N, int C, int I, int O, int mode, int prune, bool tc,
                                  int64_t wsmem, uint8_t* __restrict__ prog, ProgLayout L,
                                  int16_t* __restrict__ order_out, int16_t* __restrict__ conn_rows,
                                  int32_t* __restrict__ io_rows, int32_t* __restrict__ status_out,
@@ -283,7 +283,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   if (g >= P) return;
   using KT = KeyTraits<SMALL>;
   WarpSmem<KT> s;
-  layout_warp<true, KT>(smem + warp * wsmem, N, C, split, &s);
+  layout_warp<true, KT>(smem + warp * wsmem, N, C, &s);
   const int Npad = next_pow2(N);
   const double* gn = nodes + g * (int64_t)N * 5;
   const double* gc = conns + g * (int64_t)C * 4;
@@ -577,10 +577,59 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   }
   __syncwarp();
 
+  // ---- tensor-core program eligibility (FMT_TC) -------------------------------
+  // every emitted step aggregates by sum / mean, at most 128 steps, and
+  // every step's input-edge weights have a usable block exponent
+  // (csrc/digits.cuh); the input count of each step goes to outdeg (free since
+  // the CSR build)
+  const int n_pos = recurrent ? N : n_order;
+  bool tc_ok = tc && !recurrent && I <= TC_K;
+  if (tc_ok) {
+    int bad = 0, cnt_emit = 0;
+    for (int base = 0; base < n_pos; base += 32) {
+      const int i = base + lane;
+      const int r = i < n_pos ? (int)s.order[i] : -1;
+      const bool emit = r >= 0 && (s.flags[r] & F_LIVE) && !(s.flags[r] & F_INPUT) && s.needed[r];
+      cnt_emit += __popc(__ballot_sync(0xffffffffu, emit));
+      if (emit) {
+        const double gv = gn[(int64_t)r * 5 + 3];
+        if (!(gv == (double)AGG_SUM || gv == (double)AGG_MEAN)) bad = 1;
+        double mw = 0.0;
+        int cin = 0;
+        for (int e = s.in_start[r]; e < s.in_start[r + 1]; ++e) {
+          const typename KT::E kk = s.ekey[e];
+          if (s.flags[KT::src(kk)] & F_INPUT) {
+            const double w = gc[KT::row(kk) * 4 + 3];
+            if (!isfinite(w)) bad = 1;
+            mw = fmax(mw, fabs(w));
+            ++cin;
+          }
+        }
+        if (mw != 0.0 && (mw < 0x1p-62 || mw >= 0x1p63)) bad = 1;
+        // the kernel folds the column factor cf = 2^(e - 12) into the step: hidden
+        // weights / cf and response * cf must stay normal floats
+        const int ewx = mw != 0.0 ? ilogb(mw) : 12;
+        const double up = ldexp(1.0, 12 - ewx), dn = ldexp(1.0, ewx - 12);
+        for (int e = s.in_start[r]; e < s.in_start[r + 1]; ++e) {
+          const typename KT::E kk = s.ekey[e];
+          if (!(s.flags[KT::src(kk)] & F_INPUT)) {
+            const double w = fabs(gc[KT::row(kk) * 4 + 3]) * up;
+            if (!(w < 0x1p100) || (w != 0.0 && w < 0x1p-100)) bad = 1;
+          }
+        }
+        const double rs = fabs(gn[(int64_t)r * 5 + 2]) * dn;
+        if (!(rs < 0x1p100) || (rs != 0.0 && rs < 0x1p-100)) bad = 1;
+        s.outdeg[r] = cin;
+      }
+    }
+    tc_ok = !__any_sync(0xffffffffu, bad) && cnt_emit <= 128;  // 2 x 2 x round16(steps) TMEM columns <= 512
+  }
+  __syncwarp();
+
   // ---- steps: emitted nodes sorted by (level, class, -count, position) --------
   // feed-forward: positions in the Kahn order; recurrent: rows (all nodes are
-  // state, singleton groups, no slot recycling)
-  const int n_pos = recurrent ? N : n_order;
+  // state, singleton groups, no slot recycling).  TC programs group by the
+  // hidden-edge count (input edges go to the MMA).
   int n_emit = 0, bad = 0;
   for (int base = 0; base < n_pos; base += 32) {
     const int i = base + lane;
@@ -596,13 +645,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       const int agg = (gv >= 0.0 && gv < AGG_COUNT) ? (int)gv : 0;
       const uint32_t cls = (recurrent || !(agg == AGG_SUM || agg == AGG_MEAN)) ? 1 : 0;
       uint32_t cnt = (uint32_t)(s.in_start[r + 1] - s.in_start[r]);
-      if (split) {  // split programs group by the input-edge count (outdeg: free since the CSR build)
-        int cin = 0;
-        for (int e = s.in_start[r]; e < s.in_start[r + 1]; ++e)
-          cin += (s.flags[KT::src(s.ekey[e])] & F_INPUT) ? 1 : 0;
-        s.outdeg[r] = cin;
-        cnt = (uint32_t)cin;
-      }
+      if (tc_ok) cnt -= (uint32_t)s.outdeg[r];
       const uint32_t lv = recurrent ? 0 : (uint32_t)s.lvl[r];
       s.gkey[n_emit + __popc(me & ((1u << lane) - 1))] = KT::gmake(lv, cls, cnt, (uint32_t)i);
     }
@@ -617,57 +660,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   // group formation (sequential, lane 0): same level & class, <= 4 steps, and
   // a step joins only if its list is at least half the group's longest list
   // (bounds the padded edge entries, see edge_capacity)
-  if (lane == 0 && split) {
-    // split programs: the join rule bounds the input block; the hidden block
-    // is padded to the group's longest hidden list (edge_capacity_split)
-    int ng = 0, e_total = 0;
-    int cur_lv = -1, cur_cls = -1, cur_rounds = 0;
-    auto close = [&](GroupSplit& gr) {
-      const int gw = group_width(gr.n);
-      if (!(gr.cls & GRP_GENERIC)) {
-        gr.rounds_in = (uint16_t)((gr.rounds_in + 1) & ~1);
-        gr.rounds_h = (uint16_t)((gr.rounds_h + 1) & ~1);
-      }
-      gr.e_in = (uint16_t)e_total;
-      e_total = (int)align_up(e_total + gw * gr.rounds_in, 8);
-      gr.e_h = (uint16_t)e_total;
-      e_total = (int)align_up(e_total + gw * gr.rounds_h, 8);
-    };
-    for (int k = 0; k < n_emit; ++k) {
-      const typename KT::G key = s.gkey[k];
-      const int pos = KT::gpos(key);
-      const int row = (int)s.order[pos];
-      const int cin = KT::gcnt(key);
-      const int ch = s.in_start[row + 1] - s.in_start[row] - cin;
-      const int cls = KT::gcls(key);
-      const int lv = KT::glv(key);
-      const bool join = ng > 0 && lv == cur_lv && cls == cur_cls && cls == 0 && s.grps[ng - 1].n < 4 &&
-                        TNEAT_JOIN_DEN * cin >= TNEAT_JOIN_NUM * cur_rounds;
-      if (!join) {
-        if (ng > 0) close(s.grps[ng - 1]);
-        GroupSplit gr;
-        memset(&gr, 0, sizeof(gr));
-        gr.cls = (uint8_t)cls;
-        gr.rounds_in = (uint16_t)cin;
-        gr.step_begin = (uint16_t)k;
-        s.grps[ng++] = gr;
-        cur_lv = lv; cur_cls = cls; cur_rounds = cin;
-      }
-      GroupSplit& gr = s.grps[ng - 1];
-      gr.cnt_in[gr.n] = (uint16_t)cin;
-      gr.cnt_h[gr.n] = (uint16_t)ch;
-      if (ch > gr.rounds_h) gr.rounds_h = (uint16_t)ch;
-      const bool tanh_sum = (s.flags[row] & F_TANH_SUM) != 0;
-      if (gr.n == 0) gr.cls |= tanh_sum ? GRP_TANH_SUM : 0;
-      else if (!tanh_sum) gr.cls &= ~GRP_TANH_SUM;
-      gr.n++;
-      s.step_row[k] = (uint16_t)row;
-      s.grp_of[k] = (uint16_t)(ng - 1);
-    }
-    if (ng > 0) close(s.grps[ng - 1]);
-    s.ready[0] = (uint32_t)ng;
-    s.indeg[0] = e_total;
-  } else if (lane == 0) {
+  if (lane == 0) {
     int ng = 0, e_total = 0;
     int cur_lv = -1, cur_cls = -1, cur_rounds = 0;
     // a sum group of 3 whose first list is the longest gives the spare column
@@ -721,132 +714,115 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   const int n_groups = (int)s.ready[0];
   const int e_total = s.indeg[0];
 
-  // ---- liveness: last group reading each node ---------------------------------
-  for (int r = lane; r < N; r += 32)
-    s.last_grp[r] = (recurrent || (s.flags[r] & F_OUTPUT)) ? NEVER : -1;
-  __syncwarp();
-  if (!recurrent) {
-    for (int k = lane; k < n_emit; k += 32) {
-      const int row = s.step_row[k];
-      const int gk = s.grp_of[k];
-      for (int e = s.in_start[row]; e < s.in_start[row + 1]; ++e)
-        atomicMax(&s.last_grp[KT::src(s.ekey[e])], gk);
+  int n_slots;
+  uint16_t scratch_slot = NO_SLOT;
+  uint32_t zero_slot;
+  if (tc_ok) {
+    // TC programs: one slot per step (the MMA epilogue writes every step's input
+    // partial before the sweep), slot = step index, zero slot = n_steps
+    for (int k = lane; k < n_emit; k += 32) s.slot_of[s.step_row[k]] = (uint16_t)k;
+    zero_slot = (uint32_t)n_emit;
+    n_slots = n_emit + 1;
+    __syncwarp();
+  } else {
+    // ---- liveness: last group reading each node -------------------------------
+    for (int r = lane; r < N; r += 32)
+      s.last_grp[r] = (recurrent || (s.flags[r] & F_OUTPUT)) ? NEVER : -1;
+    __syncwarp();
+    if (!recurrent) {
+      for (int k = lane; k < n_emit; k += 32) {
+        const int row = s.step_row[k];
+        const int gk = s.grp_of[k];
+        for (int e = s.in_start[row]; e < s.in_start[row + 1]; ++e)
+          atomicMax(&s.last_grp[KT::src(s.ekey[e])], gk);
+      }
     }
-  }
-  // slots: 0..I-1 hold the inputs, the rest start free; one more slot after
-  // the last allocated one is the zero slot read by padding entries
-  // (split programs: inputs take no slot, hidden slots number from 0)
-  const int WS = (N + 2 + 31) / 32;
-  const int first_free = split ? 0 : I;
-  for (int w = lane; w < WS; w += 32) {
-    uint32_t m = 0;
-    for (int b = 0; b < 32; ++b) {
-      const int sl = w * 32 + b;
-      if (sl >= first_free && sl < N + 2) m |= 1u << b;
+    // slots: 0..I-1 hold the inputs, the rest start free; one more slot after
+    // the last allocated one is the zero slot read by padding entries
+    const int WS = (N + 2 + 31) / 32;
+    for (int w = lane; w < WS; w += 32) {
+      uint32_t m = 0;
+      for (int b = 0; b < 32; ++b) {
+        const int sl = w * 32 + b;
+        if (sl >= I && sl < N + 2) m |= 1u << b;
+      }
+      s.freemask[w] = m;
     }
-    s.freemask[w] = m;
-  }
-  if (!split)
     for (int r = lane; r < N; r += 32)
       if (s.flags[r] & F_INPUT) s.slot_of[r] = (uint16_t)gn[(int64_t)r * 5];
-  __syncwarp();
-  int n_slots = first_free;
-  for (int gi = 0; gi < n_groups; ++gi) {
-    // recycle the slots whose last reader is this group (reads precede writes)
-    if (!recurrent) {
-      for (int r = lane; r < N; r += 32) {
-        const uint16_t sl = s.slot_of[r];
-        if (sl != NO_SLOT && !(s.flags[r] & (F_OUTPUT | F_FREED)) && s.last_grp[r] <= gi) {
-          s.flags[r] |= F_FREED;
-          atomicOr(&s.freemask[sl >> 5], 1u << (sl & 31));
+    __syncwarp();
+    n_slots = I;
+    for (int gi = 0; gi < n_groups; ++gi) {
+      // recycle the slots whose last reader is this group (reads precede writes)
+      if (!recurrent) {
+        for (int r = lane; r < N; r += 32) {
+          const uint16_t sl = s.slot_of[r];
+          if (sl != NO_SLOT && !(s.flags[r] & (F_OUTPUT | F_FREED)) && s.last_grp[r] <= gi) {
+            s.flags[r] |= F_FREED;
+            atomicOr(&s.freemask[sl >> 5], 1u << (sl & 31));
+          }
         }
+        __syncwarp();
       }
-      __syncwarp();
-    }
-    const int gn_steps = split ? s.grps[gi].n : s.grp[gi].n;
-    const int g_begin = split ? s.grps[gi].step_begin : s.grp[gi].step_begin;
-    for (int j = 0; j < gn_steps; ++j) {
-      const int row = s.step_row[g_begin + j];
-      if (!(s.used[row] || (s.flags[row] & F_OUTPUT))) continue;
-      const int sl = warp_first_set(s.freemask, WS);
-      __syncwarp();
-      if (lane == 0) {
-        s.freemask[sl >> 5] &= ~(1u << (sl & 31));
-        s.slot_of[row] = (uint16_t)sl;
+      const int gn_steps = s.grp[gi].n;
+      const int g_begin = s.grp[gi].step_begin;
+      for (int j = 0; j < gn_steps; ++j) {
+        const int row = s.step_row[g_begin + j];
+        if (!(s.used[row] || (s.flags[row] & F_OUTPUT))) continue;
+        const int sl = warp_first_set(s.freemask, WS);
+        __syncwarp();
+        if (lane == 0) {
+          s.freemask[sl >> 5] &= ~(1u << (sl & 31));
+          s.slot_of[row] = (uint16_t)sl;
+        }
+        n_slots = max(n_slots, sl + 1);
+        __syncwarp();
       }
-      n_slots = max(n_slots, sl + 1);
-      __syncwarp();
     }
-  }
-  // steps whose value nobody reads (unpruned programs) write a scratch slot:
-  // every step has a slot, so kernels store step results unconditionally
-  bool orphan = false;
-  for (int k = lane; k < n_emit; k += 32) {
-    const int row = s.step_row[k];
-    orphan |= !(s.used[row] || (s.flags[row] & F_OUTPUT));
-  }
-  orphan = __any_sync(0xffffffffu, orphan);
-  const uint16_t scratch_slot = orphan ? (uint16_t)n_slots : NO_SLOT;
-  if (orphan) n_slots += 1;
-  const uint32_t zero_slot = (uint32_t)n_slots;
-  n_slots += 1;
-  // ---- write groups, steps and interleaved edge lists --------------------------
-  StepT<T>* steps = (StepT<T>*)(gp + L.off_steps);
-  if (split) {
-    GroupSplit* pg = (GroupSplit*)(gp + L.off_groups);
-    for (int gi = lane; gi < n_groups; gi += 32) pg[gi] = s.grps[gi];
-    uint16_t* esrc = (uint16_t*)(gp + L.off_src);
-    float* ew = (float*)(gp + L.off_w);
+    // steps whose value nobody reads (unpruned programs) write a scratch slot:
+    // every step has a slot, so kernels store step results unconditionally
+    bool orphan = false;
     for (int k = lane; k < n_emit; k += 32) {
       const int row = s.step_row[k];
-      const GroupSplit gr = s.grps[s.grp_of[k]];
-      const int j = k - gr.step_begin, gw = group_width(gr.n);
-      const double* nr = gn + (int64_t)row * 5;
-      const double av = nr[4], gv = nr[3];
-      StepT<T> st;
-      memset(&st, 0, sizeof(st));
-      const int e0 = s.in_start[row], cnt = s.in_start[row + 1] - e0;
-      st.slot = (s.used[row] || (s.flags[row] & F_OUTPUT)) ? s.slot_of[row] : scratch_slot;
-      st.act = (uint8_t)((av >= 0.0 && av < ACT_COUNT) ? (int)av : 0);
-      st.agg = (uint8_t)((gv >= 0.0 && gv < AGG_COUNT) ? (int)gv : 0);
-      st.count = (uint16_t)cnt;
-      st.bias = (T)nr[1];
-      st.resp = (T)nr[2];
-      steps[k] = st;
-      // holes: input block -> (input 0, 0.0), hidden block -> (zero slot, 0.0);
-      // the spare column of a 3-group is all holes
-      const int ncol = (gr.n == 3 && j == 2) ? 2 : 1;
-      for (int col = j; col < j + ncol; ++col) {
-        for (int rr = 0; rr < gr.rounds_in; ++rr) {
-          esrc[gr.e_in + rr * gw + col] = 0;
-          ew[gr.e_in + rr * gw + col] = 0.0f;
-        }
-        for (int rr = 0; rr < gr.rounds_h; ++rr) {
-          esrc[gr.e_h + rr * gw + col] = (uint16_t)zero_slot;
-          ew[gr.e_h + rr * gw + col] = 0.0f;
-        }
-      }
-      int ri = 0, rh = 0;  // source-row order inside each block
-      for (int e = e0; e < e0 + cnt; ++e) {
-        const typename KT::E kk = s.ekey[e];
-        const int sr = KT::src(kk);
-        const float w = (float)gc[KT::row(kk) * 4 + 3];
-        if (s.flags[sr] & F_INPUT) {
-          const int idx = gr.e_in + (ri++) * gw + j;
-          esrc[idx] = (uint16_t)gn[(int64_t)sr * 5];
-          ew[idx] = w;
-        } else {
-          const int idx = gr.e_h + (rh++) * gw + j;
-          esrc[idx] = s.slot_of[sr];
-          ew[idx] = w;
-        }
-      }
+      orphan |= !(s.used[row] || (s.flags[row] & F_OUTPUT));
+    }
+    orphan = __any_sync(0xffffffffu, orphan);
+    scratch_slot = orphan ? (uint16_t)n_slots : NO_SLOT;
+    if (orphan) n_slots += 1;
+    zero_slot = (uint32_t)n_slots;
+    n_slots += 1;
+  }
+
+  // TC programs: input-edge list starts (exclusive scan of the input counts in
+  // step order; lvl / last_grp are free now)
+  if (tc_ok) {
+    for (int k = lane; k < n_emit; k += 32) s.lvl[k] = s.outdeg[s.step_row[k]];
+    __syncwarp();
+    warp_exclusive_scan(s.lvl, s.last_grp, n_emit);
+    uint16_t* in_start = (uint16_t*)(gp + L.off_in);
+    for (int k = lane; k <= n_emit; k += 32) in_start[k] = (uint16_t)s.last_grp[k];
+  }
+
+  // ---- write groups, steps and interleaved edge lists --------------------------
+  // (TC programs: into the staged block, common.cuh tc_block)
+  const TcBlock tb = tc_block(n_emit, n_groups, e_total);
+  uint8_t* const blk = gp + L.off_tc;
+  StepT<T>* steps = (StepT<T>*)(tc_ok ? blk + tb.st : gp + L.off_steps);
+  GroupRec* pg = (GroupRec*)(tc_ok ? blk + tb.gr : gp + L.off_groups);
+  for (int gi = lane; gi < n_groups; gi += 32) {
+    if (tc_ok) {
+      const GroupRec r = s.grp[gi];
+      GroupTC t;
+      t.code = (uint32_t)(r.n - 1) | ((r.cls & GRP_TANH_SUM) ? 4u : 0u) | ((r.cls & GRP_SPLIT0) ? 8u : 0u);
+      t.rounds = r.rounds;
+      t.e_begin = r.e_begin;
+      t.step_begin = r.step_begin;
+      ((GroupTC*)pg)[gi] = t;
+    } else {
+      pg[gi] = s.grp[gi];
     }
   }
-  GroupRec* pg = (GroupRec*)(gp + L.off_groups);
-  if (!split)
-    for (int gi = lane; gi < n_groups; gi += 32) pg[gi] = s.grp[gi];
-  for (int k = lane; k < n_emit && !split; k += 32) {
+  for (int k = lane; k < n_emit; k += 32) {
     const int row = s.step_row[k];
     const GroupRec gr = s.grp[s.grp_of[k]];
     const int j = k - gr.step_begin, gw = group_width(gr.n);
@@ -855,17 +831,87 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     StepT<T> st;
     memset(&st, 0, sizeof(st));
     const int e0 = s.in_start[row], cnt = s.in_start[row + 1] - e0;
-    st.slot = (s.used[row] || (s.flags[row] & F_OUTPUT)) ? s.slot_of[row] : scratch_slot;
+    st.slot = tc_ok ? (uint16_t)k : ((s.used[row] || (s.flags[row] & F_OUTPUT)) ? s.slot_of[row] : scratch_slot);
     st.act = (uint8_t)((av >= 0.0 && av < ACT_COUNT) ? (int)av : 0);
     st.agg = (uint8_t)((gv >= 0.0 && gv < AGG_COUNT) ? (int)gv : 0);
     st.count = (uint16_t)cnt;
     st.bias = (T)nr[1];
     st.resp = (T)nr[2];
+    if (tc_ok) {
+      // TC programs: the step's accumulator runs divided by its column factor
+      // cf = 2^(e - 12) (the MMA epilogue then skips one multiply per step), so
+      // the response carries cf; tanh groups also pre-scale by -2 log2(e)
+      // (common.cuh GroupTC).  Powers of two: bit-identical results.
+      double mw = 0.0;
+      for (int e = e0; e < e0 + cnt; ++e) {
+        const typename KT::E kk = s.ekey[e];
+        if (s.flags[KT::src(kk)] & F_INPUT) mw = fmax(mw, fabs(gc[KT::row(kk) * 4 + 3]));
+      }
+      const double cfk = ldexp(1.0, (mw != 0.0 ? ilogb(mw) : 12) - 12);
+      const double kk = (gr.cls & GRP_TANH_SUM) ? (double)TANH_K : 1.0;
+      st.bias = (T)(nr[1] * kk);
+      st.resp = (T)(nr[2] * cfk * kk);
+    }
     steps[k] = st;
     // column j of the group's edge block; holes (and the spare column of a
     // 3-group) are (zero slot, 0.0) entries; GRP_SPLIT0: step 0's list goes
     // to columns 0 (first cnt[0] edges) and 3 (the rest)
     const bool split0 = (gr.cls & GRP_SPLIT0) != 0;
+    if constexpr (sizeof(T) == 4) {
+      if (tc_ok) {
+        // hidden edges into the interleaved block (sources as byte offsets of
+        // the kernel's slot rows), input edges into the (input index, weight)
+        // list of the exact path and the B operand row
+        uint32_t* esrc = (uint32_t*)(blk + tb.src);
+        float* ew = (float*)(blk + tb.w);
+        const int ncol = (gr.n == 3 && j == 2 && !split0) || (split0 && j == 0) ? 2 : 1;
+        for (int ci = 0; ci < ncol; ++ci) {
+          const int col = ci == 0 ? j : 3;
+          for (int rr = 0; rr < gr.rounds; ++rr) {
+            esrc[gr.e_begin + rr * gw + col] = zero_slot * TC_SLOT_BYTES;
+            ew[gr.e_begin + rr * gw + col] = 0.0f;
+          }
+        }
+        uint16_t* isrc = (uint16_t*)(gp + L.off_isrc);
+        float* iw = (float*)(gp + L.off_iw);
+        uint8_t* brow = blk + tb.b;
+        double mw = 0.0;
+        for (int e = e0; e < e0 + cnt; ++e) {
+          const typename KT::E kk = s.ekey[e];
+          if (s.flags[KT::src(kk)] & F_INPUT) mw = fmax(mw, fabs(gc[KT::row(kk) * 4 + 3]));
+        }
+        const int ewx = mw != 0.0 ? ilogb(mw) : 12;
+        const double sc = ldexp(1.0, 27 - ewx), up = ldexp(1.0, 12 - ewx);
+        ((float*)(blk + tb.cf))[k] = pow2f(12 - ewx);  // 1 / cf (the exact path's partials)
+#pragma unroll 1
+        for (int q = 0; q < 12; ++q) *(uint4*)(brow + tc_offset(k, 8 * q)) = make_uint4(0, 0, 0, 0);
+        int hc = 0, ic = s.last_grp[k];
+        const int c0 = gr.cnt[0];
+        for (int e = e0; e < e0 + cnt; ++e) {
+          const typename KT::E kk = s.ekey[e];
+          const int sr = KT::src(kk);
+          const double w = gc[KT::row(kk) * 4 + 3];
+          if (s.flags[sr] & F_INPUT) {
+            const int idx = (int)gn[(int64_t)sr * 5];
+            isrc[ic] = (uint16_t)idx;
+            iw[ic] = (float)w;
+            ++ic;
+            double d2, d1, d0;
+            digits3_d(w * sc, d2, d1, d0);
+            *(__half*)(brow + tc_offset(k, idx)) = __double2half(d2);
+            *(__half*)(brow + tc_offset(k, TC_K + idx)) = __double2half(d1);
+            *(__half*)(brow + tc_offset(k, 2 * TC_K + idx)) = __double2half(d0);
+          } else {
+            int col = j, rr = hc;
+            if (split0 && j == 0 && hc >= c0) { col = 3; rr = hc - c0; }
+            esrc[gr.e_begin + rr * gw + col] = (uint32_t)s.slot_of[sr] * TC_SLOT_BYTES;
+            ew[gr.e_begin + rr * gw + col] = (float)(w * up);
+            ++hc;
+          }
+        }
+        continue;
+      }
+    }
     int cols[2] = {j, 3}, first[2] = {0, 0}, nedge[2] = {cnt, 0};
     int ncol = (gr.n == 3 && j == 2 && !split0) ? 2 : 1;
     if (split0 && j == 0) {
@@ -908,13 +954,20 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       }
     }
   }
+  if (tc_ok) {  // B rows past the last step up to the MMA's N (multiple of 16) are zero
+    uint8_t* bp = blk + tb.b;
+    float* cf = (float*)(blk + tb.cf);
+    for (int k = n_emit + lane; k < tc_rows(n_emit); k += 32) cf[k] = 0.0f;
+    for (int k = n_emit + lane; k < tc_rows(n_emit); k += 32)
+      for (int q = 0; q < 12; ++q) *(uint4*)(bp + tc_offset(k, 8 * q)) = make_uint4(0, 0, 0, 0);
+  }
   uint16_t* out_slot = (uint16_t*)(gp + L.off_out);
   for (int o = lane; o < O; o += 32) {
     const int r = lookup_row(s.skey, Npad, (uint64_t)(I + o));
     out_slot[o] = r >= 0 ? s.slot_of[r] : NO_SLOT;
   }
   if (lane == 0) {
-    ProgHeader h{n_emit, e_total, n_slots, n_order, status, n_live, mode, n_groups};
+    ProgHeader h{n_emit, e_total, n_slots, n_order, status, n_live, tc_ok ? (int)MODE_TC : mode, n_groups};
     *hdr = h;
     if (status_out) status_out[g] = status;
     atomicMax(&maxdims[0], n_slots);
@@ -939,16 +992,16 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
                  int mode, int precision, int prune, void* program, int64_t program_stride,
                  int16_t* order, int16_t* conn_rows, int32_t* io_rows, int32_t* status,
                  int32_t* maxdims, void* stream) {
-  const bool split = (precision & FMT_SPLIT) != 0;
+  const bool tc = (precision & FMT_TC) != 0;
   if (P < 0 || N < 1 || N > 32767 || C < 0 || I < 1 || O < 1 || I + O > N) return -1;
-  if ((split ? edge_capacity_split(N, C) : edge_capacity(N, C)) > 65535) return -1;
-  if (split && ((precision & FMT_F64) || mode != 0)) return -1;  // split: fp32 feed-forward only
+  if (edge_capacity(N, C) > 65535) return -1;
+  if (tc && ((precision & FMT_F64) || mode != 0)) return -1;  // TC programs: fp32 feed-forward only
   const ProgLayout L = prog_layout(N, C, O, precision);
   if (program_stride != L.stride) return -3;
   if (P == 0) return 0;  // empty population: nothing to read or write
   if (!nodes || !program || !maxdims || (C > 0 && !conns)) return -2;
   const int Cc = C > 0 ? C : 1;
-  const int64_t ws = warp_smem_bytes(N, Cc, split);
+  const int64_t ws = warp_smem_bytes(N, Cc);
   if (ws > 200 * 1024) return -4;  // genome capacity too large for one warp's shared memory
 #ifndef TNEAT_TR_WPB
 #define TNEAT_TR_WPB 1  // one genome-warp per CTA: its shared memory is released as soon as it finishes
@@ -960,7 +1013,7 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
   cudaStream_t st = (cudaStream_t)stream;
   auto launch = [&](auto kernel) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kernel<<<(unsigned)blocks, 32 * wpb, smem, st>>>(nodes, conns, P, N, C, I, O, mode, prune, split, ws,
+    kernel<<<(unsigned)blocks, 32 * wpb, smem, st>>>(nodes, conns, P, N, C, I, O, mode, prune, tc, ws,
                                                      (uint8_t*)program, L, order, conn_rows, io_rows, status,
                                                      maxdims);
   };

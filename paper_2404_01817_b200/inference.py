@@ -18,11 +18,17 @@ path, parity ``|d| <= 1e-5 * max(1, |ref|)`` against the float64 reference;
 ``precision="f64"`` evaluates in float64 for reference-exact checking
 (<= 1e-9 like the reference's own oracle tests, test_oracle.py:82-92).
 
-Layout: ``transform_arrays(..., layout="split")`` compiles fp32 feed-forward
-programs for the split forward kernel (input values in tensor memory, hidden
-values in shared memory; csrc/forward.cu ``fwd_split_kernel``).  It is opt-in:
-``layout="auto"`` (default) gives standard programs, which every kernel takes
-(tile / warp forward, fused fitness, cart-pole, recurrent rollouts).
+Layout: ``layout="tc"`` compiles fp32 feed-forward programs for the
+tensor-core forward (csrc/forward.cu ``fwd_tc_kernel``): the input-sourced
+edges of every step become one exact digit-split tcgen05 MMA per 128-sample
+tile (csrc/digits.cuh), the hidden-sourced edges run on CUDA cores.  Genomes
+it cannot take (non-sum aggregations, out-of-range weights) get standard
+programs in the same buffer and run on the tile kernel.  ``layout="auto"``
+(default) is "tc" for fp32 feed-forward populations with I <= 32, I % 4 == 0,
+else "standard".  Standard programs run on every kernel (tile / warp forward,
+fused fitness, cart-pole, recurrent rollouts); a TC-layout population asked
+for a standard-only kernel (small batches, explicit tile variants) is
+re-transformed once into standard programs (cached).
 """
 
 from __future__ import annotations
@@ -40,9 +46,11 @@ from .functions import DEFAULT_REGISTRY, check_registry
 
 ST_CYCLIC, ST_BAD_ACT, ST_BAD_AGG, ST_BAD_KEY, ST_DANGLING, ST_MISSING_IO = 1, 2, 4, 8, 16, 32
 _PREC = {"f32": 0, "f64": 1}
-FMT_F64, FMT_SPLIT = 1, 2  # program format bits (csrc/common.cuh)
+FMT_F64, FMT_TC = 1, 2  # program format bits (csrc/common.cuh)
+MODE_TC = 2  # ProgHeader.mode of a tensor-core program
 _TORCH_DT = {0: torch.float32, 1: torch.float64, 2: torch.float32}
-V_SPLIT = 10  # forward variant of split programs (inputs in TMEM)
+V_TC = 11  # forward variant of the tensor-core kernel
+TC_MIN_BATCH = 64  # smaller batches run standard programs on the warp / tile kernels
 
 
 def _precision_code(precision) -> int:
@@ -65,7 +73,7 @@ class StackedNetworks:
     io_rows: torch.Tensor            # (P, I+O) int32
     status_dev: torch.Tensor         # (P,) int32
     maxdims: tuple[int, int, int]    # max (slots, steps, edges) over the population
-    precision: int = 0               # program format: FMT_F64 | FMT_SPLIT bits
+    precision: int = 0               # program format: FMT_F64 | FMT_TC bits
     mode: int = 0
     _cache: dict = field(default_factory=dict, repr=False)
 
@@ -159,7 +167,7 @@ class StackedNetworks:
                               self.conn_rows[idx], self.io_rows[idx], self.status_dev[idx],
                               self.maxdims, self.precision, self.mode)
         if isinstance(idx, slice):
-            for k in ("status", "slots", "steps_edges"):
+            for k in ("status", "slots", "steps_edges", "modes"):
                 if k in self._cache:
                     sub._cache[k] = self._cache[k][idx]
         return sub
@@ -230,13 +238,13 @@ def transform_arrays(nodes, conns, num_inputs: int, num_outputs: int, *,
     if nd.dim() != 3 or nd.shape[2] != 5 or cd.dim() != 3 or cd.shape[2] != 4 or nd.shape[0] != cd.shape[0]:
         raise ValueError(f"expected (P,N,5) and (P,C,4) tensors, got {tuple(nd.shape)}, {tuple(cd.shape)}")
     pop, n, c = int(nd.shape[0]), int(nd.shape[1]), int(cd.shape[1])
-    if layout not in ("auto", "split", "standard"):
-        raise ValueError(f"layout must be 'auto', 'split' or 'standard', got {layout!r}")
-    split_ok = prec == 0 and mode == 0 and 2 * num_inputs <= 512 and 7 * c + 24 * n + 16 <= 65535
-    if layout == "split" and not split_ok:
-        raise ConfigError("layout='split' needs fp32 feed-forward programs with <= 256 inputs")
-    if layout == "split":  # opt-in: measured slower than the tile kernel on config 2
-        prec |= FMT_SPLIT
+    if layout not in ("auto", "tc", "standard"):
+        raise ValueError(f"layout must be 'auto', 'tc' or 'standard', got {layout!r}")
+    tc_ok = prec == 0 and mode == 0 and num_inputs <= 32 and num_inputs % 4 == 0
+    if layout == "tc" and not tc_ok:
+        raise ConfigError("layout='tc' needs fp32 feed-forward programs with <= 32 inputs (a multiple of 4)")
+    if layout in ("tc", "auto") and tc_ok:
+        prec |= FMT_TC
     stride = int(_native.lib().an_program_stride(n, c, num_outputs, prec))
     dev = nd.device
     program = torch.empty((pop, stride), dtype=torch.uint8, device=dev)
@@ -262,16 +270,18 @@ def finalize_transform(stacked: StackedNetworks) -> np.ndarray:
     return the cyclic genome indices (feed-forward mode)."""
     md = stacked._cache.pop("maxdims_dev", None)
     if md is not None:
-        # one read-back: launch sizes, per-genome status and value-slot counts
-        # header words 0-2: steps, edge entries, value slots (common.cuh ProgHeader)
-        dims = stacked.program[:, 0:12].contiguous().view(torch.int32).reshape(-1)
+        # one read-back: launch sizes, per-genome status, value-slot counts and
+        # program formats: header words 0-2 (steps, edge entries, value slots)
+        # and 6 (mode) of common.cuh ProgHeader
+        dims = stacked.program[:, 0:28].contiguous().view(torch.int32)[:, [0, 1, 2, 6]].reshape(-1)
         host = torch.cat([md, stacked.status_dev, dims]).cpu().numpy()
         p = stacked.size
         stacked.maxdims = tuple(int(v) for v in host[:3])
         stacked._cache["status"] = host[3:3 + p]
-        d3 = host[3 + p:].reshape(p, 3)
-        stacked._cache["slots"] = d3[:, 2]
-        stacked._cache["steps_edges"] = d3[:, :2]
+        d4 = host[3 + p:].reshape(p, 4)
+        stacked._cache["slots"] = d4[:, 2]
+        stacked._cache["steps_edges"] = d4[:, :2]
+        stacked._cache["modes"] = d4[:, 3]
     return status_cyclic(stacked.status, stacked.mode)
 
 
@@ -349,45 +359,58 @@ _TILE_TT = {1: 128, 2: 256, 3: 64, 4: 256, 5: 128, 6: 128}
 _SMEM_PER_SM = 228 * 1024
 
 
-def _bucket_plan(stacked: StackedNetworks, variant: int) -> list:
-    """Occupancy buckets: genomes sorted by value-slot count and split where
-    the number of resident CTAs per SM changes; each bucket is one launch with
-    its own (tighter) shared-memory size.  Cached on the stacked object."""
-    key = ("plan", variant)
+def _host_dims(stacked: StackedNetworks) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Per-genome (slots, (steps, edges), mode) from the transform's read-back
+    (read here if the stacked object has none)."""
+    if "steps_edges" not in stacked._cache or "modes" not in stacked._cache:
+        d = stacked.program[:, 0:28].contiguous().view(torch.int32)[:, [0, 1, 2, 6]].cpu().numpy()
+        stacked._cache["slots"] = d[:, 2]
+        stacked._cache["steps_edges"] = d[:, :2]
+        stacked._cache["modes"] = d[:, 3]
+    return stacked._cache["slots"], stacked._cache["steps_edges"], stacked._cache["modes"]
+
+
+def _upload_plan(stacked: StackedNetworks, key, ids_host: np.ndarray):
+    # no stream sync (plans are made inside copy/compute pipelines); launches wait on the upload's event
+    ids, ev = upload_async(ids_host.astype(np.int32), stacked.program.device)
+    stacked._cache[("plan_ready", key)] = ev
+    stacked._cache[("plan_ids", key)] = ids
+    return ids
+
+
+def _bucket_plan(stacked: StackedNetworks, variant: int, subset: np.ndarray | None = None,
+                 key=None) -> list:
+    """Occupancy buckets of the tile kernel: genomes (all, or ``subset``)
+    sorted by value-slot count and split where the number of resident CTAs per
+    SM changes; each bucket is one launch with its own (tighter) shared-memory
+    size.  Cached on the stacked object."""
+    key = key if key is not None else ("plan", variant)
     if key in stacked._cache:
         return stacked._cache[key]
     tt = _TILE_TT.get(variant, 256)
     esz = 8 if stacked.precision & FMT_F64 else 4
-    slots = stacked._cache.get("slots")
-    if slots is None:
-        slots = stacked.program[:, 8:12].contiguous().view(torch.int32).reshape(-1).cpu().numpy()
+    slots, se, _ = _host_dims(stacked)
+    members = np.arange(slots.size, dtype=np.int64) if subset is None else subset
+    msl = slots[members]
     # slot counts are small integers: a 16-bit key makes numpy's stable sort a radix sort
-    order = np.argsort(np.minimum(slots, 65535).astype(np.uint16), kind="stable").astype(np.int32)
+    order = members[np.argsort(np.minimum(msl, 65535).astype(np.uint16), kind="stable")]
     sorted_slots = slots[order]
-    # no stream sync (plans are made inside copy/compute pipelines); launches wait on the upload's event
-    ids, ev = upload_async(order, stacked.program.device)
-    stacked._cache[("plan_ready", variant)] = ev
-    stacked._cache[("plan_ids", variant)] = ids
+    ids = _upload_plan(stacked, key, order)
     _, ms, me = stacked.maxdims
     prog = 32 * ms + (16 * me if stacked.precision & FMT_F64 else 8 * me + 16) + 16
-    if variant == V_SPLIT:  # fwd_split_kernel: 4 warps, 256 inputs per tile, hidden slots only
-        prog += 16 * ms
-        occ = np.minimum(_SMEM_PER_SM // (prog + np.maximum(sorted_slots, 1) * 258 * 4 + 1024),
-                         512 // max(32, 1 << int(np.ceil(np.log2(max(1, 2 * stacked.num_inputs))))))
-    else:
-        pad = {1: 1, 2: 2, 3: 1, 4: 4, 5: 2, 6: 4}[variant]
-        occ = _SMEM_PER_SM // (prog + np.maximum(sorted_slots, stacked.num_inputs) * (tt + pad) * esz + 1024)
-    # per-bucket program extents (steps, edge entries) when the read-back has them:
-    # a launch sizes its shared program area for its own genomes, not the population's
-    # largest (fp32 tile kernel only; the classes above stay conservative)
-    se = stacked._cache.get("steps_edges") if variant != V_SPLIT and not stacked.precision & FMT_F64 else None
+    pad = {1: 1, 2: 2, 3: 1, 4: 4, 5: 2, 6: 4}[variant]
+    occ = _SMEM_PER_SM // (prog + np.maximum(sorted_slots, stacked.num_inputs) * (tt + pad) * esz + 1024)
+    # per-bucket program extents (steps, edge entries): a launch sizes its shared
+    # program area for its own genomes, not the population's largest (fp32 tile
+    # kernel only; the classes above stay conservative)
+    fp32 = not stacked.precision & FMT_F64
     plan = []
     lo = 0
     n = sorted_slots.size
     while lo < n:
         hi = lo + int(np.searchsorted(occ[lo:] != occ[lo], True))  # first index with another class
         hi = n if hi == lo else hi
-        if se is not None:
+        if fp32:
             ext = se[order[lo:hi]].max(axis=0)
             plan.append((ids[lo:hi], (int(sorted_slots[hi - 1]), int(ext[0]), int(ext[1]))))
         else:
@@ -395,6 +418,46 @@ def _bucket_plan(stacked: StackedNetworks, variant: int) -> list:
         lo = hi
     stacked._cache[key] = plan
     return plan
+
+
+def _tc_plan(stacked: StackedNetworks) -> tuple[list, list]:
+    """Launch plan of an FMT_TC population: tensor-core programs bucketed by
+    their MMA width (steps rounded up to 16: it sets the TMEM columns and the
+    shared-memory footprint, i.e. the resident CTAs per SM), each bucket sized
+    by its own (steps, edge entries) extents; standard programs (genomes the
+    tensor-core format cannot take) go to the tile kernel's buckets."""
+    key = ("plan", V_TC)
+    if key in stacked._cache:
+        return stacked._cache[key]
+    slots, se, modes = _host_dims(stacked)
+    tc = np.nonzero(modes == MODE_TC)[0]
+    std = np.nonzero(modes != MODE_TC)[0]
+    plan_tc = []
+    if tc.size:
+        nb = (se[tc, 0] + 15) // 16
+        order = tc[np.argsort(nb, kind="stable")]
+        ids = _upload_plan(stacked, key, order)
+        snb = (se[order, 0] + 15) // 16
+        bounds = np.flatnonzero(np.diff(snb)) + 1
+        for lo, hi in zip(np.concatenate([[0], bounds]), np.concatenate([bounds, [order.size]])):
+            ext = se[order[lo:hi]].max(axis=0)
+            plan_tc.append((ids[lo:hi], (int(slots[order[lo:hi]].max()), int(ext[0]), int(ext[1]))))
+    plan_std = _bucket_plan(stacked, 5, std, key=("plan_tcstd", 5)) if std.size else []
+    stacked._cache[key] = (plan_tc, plan_std)
+    return stacked._cache[key]
+
+
+def standard_programs(stacked: StackedNetworks) -> StackedNetworks:
+    """Standard-layout programs of an FMT_TC population (for the kernels that
+    only take standard programs), transformed once and cached."""
+    if not stacked.precision & FMT_TC:
+        return stacked
+    std = stacked._cache.get("standard")
+    if std is None:
+        std, _ = transform_arrays(stacked.nodes_dev, stacked.conns_dev, stacked.num_inputs, stacked.num_outputs,
+                                  network_type="feedforward", layout="standard")
+        stacked._cache["standard"] = std
+    return std
 
 
 def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Tensor | None = None,
@@ -424,23 +487,38 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
           or tuple(out.shape) != (pop, b, stacked.num_outputs) or out.device != inputs.device):
         raise ValueError(f"out must be a contiguous CUDA {dt} tensor of shape (P={pop}, B={b}, "
                          f"O={stacked.num_outputs}) on {inputs.device}")
-    if stacked.precision & FMT_SPLIT:
-        v = (variant & 0xF) or V_SPLIT
-        if v != V_SPLIT:
-            raise ValueError(f"split programs run on the split kernel only (variant {V_SPLIT}); transform "
-                             f"with layout='standard' for variant {v}")
-    else:
-        v = (variant & 0xF) or (5 if b >= 192 else (3 if b >= 96 else 8))
+    if stacked.precision & FMT_TC:
+        v = variant & 0xF
+        if v not in (0, V_TC) or (v == 0 and b < TC_MIN_BATCH) or not bucketed:
+            # standard-only kernels (or an unbucketed launch): standard programs
+            return forward_device(standard_programs(stacked), inputs, out, shared=shared, variant=variant,
+                                  bucketed=bucketed, stream=stream)
+        plan_tc, plan_std = _tc_plan(stacked)
+        launch = stream or torch.cuda.current_stream()
+        args = (ptr(stacked.program), stacked.stride, stacked.max_nodes, stacked.max_conns, stacked.precision)
+        tpc = variant & 0xFF00
+        for key, plan, vv in ((("plan", V_TC), plan_tc, V_TC), (("plan_tcstd", 5), plan_std, 5)):
+            if not plan:
+                continue
+            launch.wait_event(stacked._cache[("plan_ready", key)])
+            if launch != torch.cuda.current_stream():
+                stacked._cache[("plan_ids", key)].record_stream(launch)
+            for ids, md in plan:
+                _native.call("an_forward", *args, _maxdims_arg(stacked, md), ptr(ids), ptr(inputs), gstride,
+                             int(ids.numel()), b, i, stacked.num_outputs, ptr(out), vv | tpc,
+                             stream_handle(stream))
+        return out
+    v = (variant & 0xF) or (5 if b >= 192 else (3 if b >= 96 else 8))
     args = (ptr(stacked.program), stacked.stride, stacked.max_nodes, stacked.max_conns, stacked.precision)
     tail = (b, i, stacked.num_outputs, ptr(out), int(variant) if variant > 15 else int(v),
             stream_handle(stream))
     v &= 0xF
-    if (v in _TILE_TT or v == V_SPLIT) and bucketed and pop > 1:
+    if v in _TILE_TT and bucketed and pop > 1:
         plan = _bucket_plan(stacked, v)
         launch = stream or torch.cuda.current_stream()
-        launch.wait_event(stacked._cache[("plan_ready", v)])
+        launch.wait_event(stacked._cache[("plan_ready", ("plan", v))])
         if launch != torch.cuda.current_stream():
-            stacked._cache[("plan_ids", v)].record_stream(launch)  # allocated on the current stream
+            stacked._cache[("plan_ids", ("plan", v))].record_stream(launch)  # allocated on the current stream
         for ids, md in plan:
             _native.call("an_forward", *args, _maxdims_arg(stacked, md), ptr(ids), ptr(inputs), gstride,
                          int(ids.numel()), *tail)
@@ -485,8 +563,7 @@ def _host_forward_pipelined(stacked: StackedNetworks, x: torch.Tensor, out_host:
     dt = _TORCH_DT[stacked.precision]
     dev = device()
     per = max(1, int(chunk_bytes // max(1, b * i * x.element_size())))
-    if "slots" not in stacked._cache:
-        stacked._cache["slots"] = stacked.program[:, 8:12].contiguous().view(torch.int32).reshape(-1).cpu().numpy()
+    _host_dims(stacked)
     bufs_in = [torch.empty((min(per, pop), b, i), dtype=dt, device=dev) for _ in range(2)]
     bufs_out = [torch.empty((min(per, pop), b, o), dtype=dt, device=dev) for _ in range(2)]
     h2d, comp, d2h = torch.cuda.Stream(), torch.cuda.current_stream(), torch.cuda.Stream()

@@ -1,9 +1,11 @@
 """Parity of the exact benchmarked launch (bench.py's step, BASELINE configs[1]).
 
 The bench transforms the §8d population (pop 10,000, 128/512, I=32, O=8,
-seed 20261018, tanh/sum) and runs the bucketed tile forward over 4096 inputs
-per genome generated on the device (seed 20261019).  This test makes the same
-calls, checks the plan forms every occupancy bucket the bench launches, and
+seed 20261018, tanh/sum) and runs the bucketed tensor-core forward
+(fwd_tc_kernel, one launch per MMA-width class) over 4096 inputs per genome
+generated on the device (seed 20261019).  This test makes the same calls,
+checks every genome takes the tensor-core format and the plan forms the
+buckets the bench launches, and
 compares a stratified 256-genome subset -- every bucket represented -- across
 all 4096 inputs with the oracle at |d| <= 1e-5 * max(1, |ref|) (north_star's
 fp32 bound).  It also checks the step's second half: the next transform on
@@ -43,18 +45,24 @@ def bench_run():
     return tn, st, nodes_h, conns_h, x, out
 
 
+def _plan(tn, st):
+    plan_tc, plan_std = st._cache[("plan", tn.inference.V_TC)]
+    return plan_tc, plan_std
+
+
 def test_bench_plan_has_every_bucket(bench_run):
     tn, st, *_ = bench_run
-    plan = st._cache[("plan", 5)]
+    plan, plan_std = _plan(tn, st)
+    assert not plan_std  # every tanh/sum genome takes the tensor-core format
     sizes = [int(ids.numel()) for ids, _ in plan]
     assert sum(sizes) == POP
-    assert len(plan) >= 4, sizes  # the bench's pass is 5 occupancy classes (profiles/r01_bench_launches.csv)
+    assert len(plan) >= 4, sizes  # MMA-width classes of 16 steps: 16..80
 
 
 def test_bench_launch_matches_oracle_on_stratified_subset(bench_run):
     from oracle import arrayneat_oracle as orc
     tn, st, nodes_h, conns_h, x, out = bench_run
-    plan = st._cache[("plan", 5)]
+    plan, _ = _plan(tn, st)
     rng = np.random.default_rng(7)
     per = -(-256 // len(plan))
     picks = []

@@ -7,8 +7,8 @@ Tolerances (written here, per north_star):
   * f32 programs: |d| <= 1e-5 * max(1, |ref|) (north_star) on
     tanh/sum and mixed act/agg networks alike (profiles/r02_parity_report.json:
     max 2.4e-6 over 3.2M checked outputs).  Both program layouts --
-    "standard" (tile / warp kernels) and "split" (inputs in tensor memory,
-    fwd_split_kernel) -- meet the same bounds.
+    "standard" (tile / warp kernels) and "tc" (input layer as an exact
+    digit-split tcgen05 MMA, fwd_tc_kernel) -- meet the same bounds.
 """
 
 from __future__ import annotations
@@ -73,11 +73,14 @@ def test_forward_f32_matches_reference(tn, name, tol):
     for variant in (0, 1, 2, 4, 8):
         out = tn.forward_arrays(st, None, x, variant=variant)
         assert _rel_err(out, ref) <= tol, (variant, _rel_err(out, ref))
-    sp, _ = tn.transform_arrays(g["nodes"][ok], g["conns"][ok], int(g["num_inputs"]),
-                                int(g["num_outputs"]), layout="split")
-    assert sp.precision & tn.inference.FMT_SPLIT
-    out = tn.forward_arrays(sp, None, x)
-    assert _rel_err(out, ref) <= tol, ("split", _rel_err(out, ref))
+    ni = int(g["num_inputs"])
+    if ni <= 32 and ni % 4 == 0:
+        import torch
+        sp, _ = tn.transform_arrays(g["nodes"][ok], g["conns"][ok], ni, int(g["num_outputs"]), layout="tc")
+        assert sp.precision & tn.inference.FMT_TC
+        out = tn.forward_device(sp, torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda(),
+                                variant=tn.inference.V_TC).cpu().numpy()
+        assert _rel_err(out, ref) <= tol, ("tc", _rel_err(out, ref))
 
 
 def test_tile_variants_bitwise_equal_and_chunk_invariant(tn):
@@ -96,14 +99,16 @@ def test_tile_variants_bitwise_equal_and_chunk_invariant(tn):
     assert torch.equal(half, outs[1][:, 300:700])
 
 
-def test_split_chunk_invariant_and_matches_standard(tn):
-    """Split programs: genome chunks / input sub-ranges / shared inputs give
-    bitwise identical rows; results agree with the standard layout to fp32."""
+def test_tc_chunk_invariant_and_matches_standard(tn):
+    """Tensor-core programs: genome chunks / input sub-ranges / shared inputs
+    give bitwise identical rows; results agree with the standard layout to fp32;
+    every genome of the tanh/sum population takes the tensor-core format."""
     import torch
     from oracle.arrayneat_oracle import synthetic_population
     nodes, conns = synthetic_population(40, 128, 512, 32, 8, seed=78)
-    sp, _ = tn.transform_arrays(nodes, conns, 32, 8, layout="split")
+    sp, _ = tn.transform_arrays(nodes, conns, 32, 8, layout="tc")
     st, _ = tn.transform_arrays(nodes, conns, 32, 8, layout="standard")
+    assert (sp._cache["modes"] == tn.inference.MODE_TC).all()
     x = torch.randn(40, 1000, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(2))
     full = tn.forward_device(sp, x)
     part = torch.cat([tn.forward_device(sp.select(slice(a, a + 13)), x[a:a + 13].contiguous())
@@ -117,15 +122,15 @@ def test_split_chunk_invariant_and_matches_standard(tn):
     assert torch.equal(shared[0], full[0])
 
 
-@pytest.mark.parametrize("ni", [1, 3, 5, 12, 40, 64])
-def test_split_input_widths(tn, ni):
-    """TMEM column layouts for odd / small / wide input counts, scalar and
-    vector input loads, against the oracle."""
+@pytest.mark.parametrize("ni", [4, 8, 12, 28, 32])
+def test_tc_input_widths(tn, ni):
+    """Input counts below the 32-wide K plane (zero-filled by the TMA box) and
+    ragged batches, against the oracle."""
     import torch
     from oracle import arrayneat_oracle as orc
     nodes, conns = orc.synthetic_population(12, 48 + ni, 160, ni, 3, seed=100 + ni, min_conns=20,
                                             max_conns_drawn=150)
-    sp, cyc = tn.transform_arrays(nodes, conns, ni, 3, layout="split")
+    sp, cyc = tn.transform_arrays(nodes, conns, ni, 3, layout="tc")
     assert cyc.size == 0
     x = np.random.default_rng(ni).standard_normal((12, 300, ni), dtype=np.float32)
     out = tn.forward_device(sp, torch.from_numpy(x).cuda()).cpu().numpy()
@@ -135,22 +140,48 @@ def test_split_input_widths(tn, ni):
         assert _rel_err(out[p], ref) <= 1e-5, (p, _rel_err(out[p], ref))
 
 
-def test_split_nonfinite_inputs_match_standard(tn):
-    """A tile with an infinite input runs the exact variant (no 0 * inf from
-    padding): outputs equal the standard layout's, NaN/inf positions included."""
+def test_tc_nonfinite_and_extreme_inputs_match_standard(tn):
+    """Rows with an infinite input, or a max |x| outside the digit scaling
+    range, take the exact path: outputs equal the standard layout's to fp32,
+    NaN/inf positions included."""
     import torch
     from oracle.arrayneat_oracle import synthetic_population
     nodes, conns = synthetic_population(6, 128, 512, 32, 8, seed=79)
-    sp, _ = tn.transform_arrays(nodes, conns, 32, 8, layout="split")
+    sp, _ = tn.transform_arrays(nodes, conns, 32, 8, layout="tc")
     st, _ = tn.transform_arrays(nodes, conns, 32, 8, layout="standard")
     x = torch.randn(6, 600, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(3))
     x[1, 17, 5] = float("inf")
     x[4, 300, 0] = -float("inf")
+    x[2, 5] *= 1e-20  # tiny row (exponent < -62)
+    x[3, 9, 7] = 1e30  # huge entry (exponent > 62)
+    x[5, 11] = 0.0  # all-zero row
     a = tn.forward_device(sp, x)
     b = tn.forward_device(st, x, variant=2)
     assert torch.equal(torch.isnan(a), torch.isnan(b))
     fin = ~torch.isnan(a)
+    assert torch.equal(torch.isinf(a), torch.isinf(b))
+    fin = fin & ~torch.isinf(a)
     assert (a[fin] - b[fin]).abs().max().item() <= 2e-5
+
+
+def test_tc_mixed_population_routes_standard_programs(tn):
+    """Genomes the tensor-core format cannot take (non-sum aggregations) get
+    standard programs in the same buffer and run on the tile kernel."""
+    import torch
+    from oracle import arrayneat_oracle as orc
+    nt, ct = orc.synthetic_population(8, 128, 512, 32, 8, seed=80)
+    nm, cm = orc.synthetic_population(8, 128, 512, 32, 8, seed=81, variant="M")
+    nodes, conns = np.concatenate([nt, nm]), np.concatenate([ct, cm])
+    sp, cyc = tn.transform_arrays(nodes, conns, 32, 8, layout="tc")
+    assert cyc.size == 0
+    modes = sp._cache["modes"]
+    assert (modes[:8] == tn.inference.MODE_TC).all() and (modes[8:] != tn.inference.MODE_TC).any()
+    x = np.random.default_rng(5).standard_normal((16, 512, 32), dtype=np.float32)
+    out = tn.forward_device(sp, torch.from_numpy(x).cuda()).cpu().numpy()
+    for p in range(16):
+        tr = orc.transform_genome(nodes[p], conns[p], 32, 8)
+        ref = orc.forward_genome(nodes[p], tr, x[p].astype(np.float64))
+        assert _rel_err(out[p], ref) <= 1e-5, (p, _rel_err(out[p], ref))
 
 
 def test_config2_shapes_against_oracle_sampled(tn):

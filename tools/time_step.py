@@ -33,8 +33,11 @@ for rep in range(a.reps):
     t1 = time.perf_counter()
     tn.finalize_transform(st)
     t2 = time.perf_counter()
-    v = (a.variant & 0xF) or (10 if st.precision & 2 else 5)
-    plan = tn.inference._bucket_plan(st, v)
+    if st.precision & tn.inference.FMT_TC:
+        pt, ps = tn.inference._tc_plan(st)
+        plan = pt + ps
+    else:
+        plan = tn.inference._bucket_plan(st, (a.variant & 0xF) or 5)
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     tn.forward_device(st, x, out, variant=a.variant)
