@@ -29,8 +29,11 @@ extern "C" {
 
 /* Bytes of one genome's compiled program for capacity (N nodes, C conns, O
  * outputs).  `precision` is the program format: bit 0 = fp64 program (else
- * fp32), bit 1 = split program (fp32 feed-forward only: input values in
- * tensor memory, see an_forward variant 10); 0 = the standard fp32 program. */
+ * fp32), bit 1 = FMT_TC (fp32 feed-forward only: genomes whose steps all
+ * aggregate by sum / mean get tensor-core programs -- the input layer as an
+ * exact digit-split tcgen05 MMA -- the others standard programs in the same
+ * stride; see an_forward variant 11 and an_forward_planned); 0 = the standard
+ * fp32 program. */
 int64_t an_program_stride(int N, int C, int O, int precision);
 
 /* Genome transform.  Replaces inference.transform_arrays
@@ -75,11 +78,35 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
  *            so a launch per slot-count bucket raises occupancy
  *   variant  0 auto, 1/3 = tile kernel 1 input/thread (128/64 threads),
  *            2/5 = 2 inputs/thread (128/64 threads), 4 = 4 inputs/thread,
- *            8 = warp-per-genome kernel (small B), 10 = split programs (the only
- *            kernel for them); bits 8..15 = tiles per CTA (0 = 4) */
+ *            8 = warp-per-genome kernel (small B), 11 = tensor-core kernel
+ *            (FMT_TC programs whose header mode is 2; persistent, one CTA per
+ *            SM; bits 8..11 = maximum warpgroups per CTA, 0 = as many as
+ *            fit).  In an FMT_TC population the other variants take the
+ *            standard-program genomes only.  Bits 8..15 = tiles per CTA for
+ *            the tile kernels (0 = 4) */
 int an_forward(const void* program, int64_t program_stride, int N, int C, int precision,
                const int32_t* maxdims_host, const int32_t* genome_ids, const void* inputs,
                int64_t input_genome_stride, int64_t P, int B, int I, int O, void* outputs, int variant,
+               void* stream);
+
+/* Forward of an FMT_TC population from a DEVICE-side launch plan: a plan
+ * kernel sorts the genomes into classes (tensor-core programs by MMA width,
+ * oversized ones, standard programs) and every launch is sized from class
+ * bounds, so no host-side counts, extents or synchronisation are needed
+ * (a transform + forward step can be enqueued ahead or graph-captured).
+ * Replaces inference.forward_arrays (inference.py:185-262) for such
+ * populations.  plan_ids int32[6 * P] and plan_counts int32[6] are DEVICE
+ * scratch owned by the caller; inputs / outputs as an_forward (float32). */
+int an_forward_planned(const void* program, int64_t program_stride, int N, int C, int precision,
+                       int32_t* plan_ids, int32_t* plan_counts, const void* inputs,
+                       int64_t input_genome_stride, int64_t P, int B, int I, int O, void* outputs,
+                       void* stream);
+
+/* The plan step of an_forward_planned alone (diagnostics): plan_counts[c] =
+ * genomes of class c (0..3 tensor-core programs with round16(steps) <= 32, 48,
+ * 64, 128; 4 tensor-core programs with > 512 hidden-edge entries; 5 standard
+ * programs), plan_ids[c * P + i] their program rows in population order. */
+int an_plan_tc(const void* program, int64_t program_stride, int64_t P, int32_t* plan_ids, int32_t* plan_counts,
                void* stream);
 
 /* Forward fused with the built-in fitness.  Replaces

@@ -21,6 +21,8 @@ SIGNATURES: dict[str, tuple] = {
     "an_program_stride": (I64, [I32, I32, I32, I32]),
     "an_transform": (I32, [P, P, I64, I32, I32, I32, I32, I32, I32, I32, P, I64, P, P, P, P, P, P]),
     "an_forward": (I32, [P, I64, I32, I32, I32, P, P, P, I64, I64, I32, I32, I32, P, I32, P]),
+    "an_forward_planned": (I32, [P, I64, I32, I32, I32, P, P, P, I64, I64, I32, I32, I32, P, P]),
+    "an_plan_tc": (I32, [P, I64, I64, P, P, P]),
     "an_forward_fitness": (I32, [P, I64, I32, I32, I32, P, P, I64, I64, I32, I32, I32, I32, P, P, P]),
     "an_cartpole": (I32, [P, I64, I32, I32, I32, P, I64, P, I32, P, P]),
     "an_rng_draw": (I32, [P, I64, U64, I64, I32, P, P]),
@@ -81,7 +83,11 @@ def call(name: str, *args) -> int:
     undeclared one would be called with C-int arguments)."""
     if name not in SIGNATURES:
         raise NativeError(f"{name} has no ctypes signature in _native.SIGNATURES")
-    ret = getattr(lib(), name)(*args)
+    return check(name, getattr(lib(), name)(*args))
+
+
+def check(name: str, ret: int) -> int:
+    """Raise NativeError for a negative status of entry point ``name``."""
     if ret < 0:
         if ret <= -100:
             raise NativeError(f"{name}: CUDA error {-(ret + 100)}")

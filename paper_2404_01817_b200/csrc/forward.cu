@@ -467,17 +467,14 @@ __device__ __forceinline__ void run_group(const GroupRec& gr, const uint32_t* sr
 // grid: one CTA per (genome, run of `tpc` consecutive tiles); the genome's
 // program is staged in shared memory once and reused for every tile
 template <typename T, int S, int NT>
-__global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const uint8_t* __restrict__ prog, ProgLayout L,
-                                                      const int32_t* __restrict__ genome_ids,
-                                                      const T* __restrict__ in, int64_t in_gstride,
-                                                      int B, int I, int O, int runs, int tpc,
-                                                      T* __restrict__ out, int64_t out_gstride) {
+__device__ __forceinline__ void tile_task(const uint8_t* __restrict__ prog, const ProgLayout& L,
+                                          const int32_t* __restrict__ genome_ids, const T* __restrict__ in,
+                                          int64_t in_gstride, int B, int I, int O, int64_t task, int run, int tpc,
+                                          T* __restrict__ out, int64_t out_gstride) {
   constexpr int TT = NT * S;
   constexpr int RB = (TT + S) * sizeof(T);  // bytes of one value slot row (padded by S)
   using PackT = Pack<T, S>;
   extern __shared__ __align__(16) uint8_t smem[];
-  const int64_t task = blockIdx.x / runs;
-  const int run = (int)(blockIdx.x - task * runs);
   const int64_t gi = genome_ids ? (int64_t)__ldg(genome_ids + task) : task;
   const uint8_t* gp = prog + gi * L.stride;
   const ProgHeader hdr = *reinterpret_cast<const ProgHeader*>(gp);
@@ -681,6 +678,31 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
   }
 }
 
+// grid: (genome, run of `tpc` consecutive tiles) tasks; with a device-side
+// genome count (count_dev, the device launch plan) the grid strides over the
+// tasks of the first *count_dev genome ids
+template <typename T, int S, int NT>
+__global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const uint8_t* __restrict__ prog, ProgLayout L,
+                                                      const int32_t* __restrict__ genome_ids,
+                                                      const int32_t* __restrict__ count_dev,
+                                                      const T* __restrict__ in, int64_t in_gstride,
+                                                      int B, int I, int O, int runs, int tpc,
+                                                      T* __restrict__ out, int64_t out_gstride) {
+  if (!count_dev) {
+    const int64_t task = blockIdx.x / runs;
+    tile_task<T, S, NT>(prog, L, genome_ids, in, in_gstride, B, I, O, task, (int)(blockIdx.x - task * runs), tpc,
+                        out, out_gstride);
+    return;
+  }
+  const int64_t n = (int64_t)__ldg(count_dev) * runs;
+  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+    if (t != blockIdx.x) __syncthreads();  // the previous task's shared memory is consumed
+    const int64_t task = t / runs;
+    tile_task<T, S, NT>(prog, L, genome_ids, in, in_gstride, B, I, O, task, (int)(t - task * runs), tpc, out,
+                        out_gstride);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // tensor-core forward (FMT_TC programs): input layer on tcgen05, hidden
 // edges on CUDA cores
@@ -874,7 +896,8 @@ struct TcShared {
 
 __global__ void __launch_bounds__(TC_NT* TC_MAX_WG, 1)
 fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __restrict__ prog, ProgLayout L,
-              const int32_t* __restrict__ genome_ids, int64_t P, const float* __restrict__ in, int64_t in_gstride,
+              const int32_t* __restrict__ genome_ids, const int32_t* __restrict__ count_dev, int64_t P,
+              const float* __restrict__ in, int64_t in_gstride,
               int B, int I, int O, int nwg, uint32_t wg_bytes, uint32_t gbuf_bytes, int nbuf, int nb_max,
               float* __restrict__ out,
               int64_t out_gstride) {
@@ -886,6 +909,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
   const int bar_id = 1 + wg;
   uint8_t* const wg_area = smem + (uint32_t)wg * wg_bytes;
   uint8_t* const gbuf0 = smem + (uint32_t)nwg * wg_bytes;
+  if (count_dev) P = __ldg(count_dev);  // device launch plan: this class's genome count
   const uint32_t slot_cols = 4u * (uint32_t)nb_max;
   const uint32_t n_slots = 512u / slot_cols;
   const int tiles = (B + TC_TT - 1) / TC_TT;
@@ -1421,23 +1445,58 @@ int launch_warp(const uint8_t* prog, const ProgLayout& L, int64_t P, const T* in
 template <typename T, int S, int NT>
 int launch_tile(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, const T* in, int64_t in_gstride,
                 int64_t P, int B, int I, int O, const int32_t* maxdims_host, T* out, int64_t out_gstride,
-                int tpc, cudaStream_t st) {
+                int tpc, cudaStream_t st, const int32_t* count_dev = nullptr) {
   constexpr int TT = NT * S;
   const int tiles = (B + TT - 1) / TT;
   tpc = max(1, min(tpc, tiles));
   const int runs = (tiles + tpc - 1) / tpc;
-  const int64_t grid = P * runs;
+  int64_t grid = P * runs;
+  if (count_dev) {  // device plan: a grid-striding launch of a few waves
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = min(grid, (int64_t)sms * 8);
+  }
   if (grid > 0x7FFFFFFFll) return -5;
+  if (grid == 0) return 0;
   const int64_t ms = maxdims_host[1], me = maxdims_host[2];
   const int64_t prog_bytes = ms * sizeof(GroupRec) + ms * sizeof(StepT<T>) +
                              (sizeof(T) == 8 ? 16 * me : align_up(4 * me, 16) + 4 * me);
   int64_t smem = align_up(prog_bytes, 16) + (int64_t)max(maxdims_host[0], I) * (TT + S) * sizeof(T);
   if (smem > 227 * 1024) return -6;
   cudaFuncSetAttribute(fwd_tile_kernel<T, S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fwd_tile_kernel<T, S, NT><<<(unsigned)grid, NT, smem, st>>>(prog, L, ids, in, in_gstride, B, I, O, runs, tpc,
+  fwd_tile_kernel<T, S, NT><<<(unsigned)grid, NT, smem, st>>>(prog, L, ids, count_dev, in, in_gstride, B, I, O, runs, tpc,
                                                               out, out_gstride);
   TNEAT_CHECK_LAUNCH();
   return 0;
+}
+
+// shared-memory configuration of a tensor-core launch whose genomes have at
+// most ms steps and me edge entries: warpgroup areas, genome buffers (two
+// unless a single one buys another warpgroup or is the only way one fits)
+struct TcConfig {
+  uint32_t wg_bytes, gbuf;
+  int nbuf, nwg;
+  int64_t smem;
+  bool ok;
+};
+inline TcConfig tc_config(int ms, int me, int max_wg) {
+  TcConfig c;
+  const int nb = tc_rows(ms);
+  c.wg_bytes = tc_wg_bytes(nb);
+  c.gbuf = (uint32_t)align_up(tc_block(ms, ms, me).bytes + 64, 128);  // + look-ahead slack
+  const int64_t budget = 227 * 1024, ctl = (int64_t)align_up(sizeof(TcShared), 16);
+  auto fit = [&](int nbuf) {
+    int w = max_wg > 0 ? min(max_wg, TC_MAX_WG) : TC_MAX_WG;
+    while (w > 1 && ctl + nbuf * (int64_t)c.gbuf + (int64_t)w * c.wg_bytes > budget) --w;
+    return w;
+  };
+  const bool two_fit = ctl + 2ll * c.gbuf + (int64_t)c.wg_bytes <= budget;
+  c.nbuf = (!two_fit || fit(1) > fit(2)) ? 1 : 2;
+  c.nwg = fit(c.nbuf);
+  c.smem = ctl + c.nbuf * (int64_t)c.gbuf + (int64_t)c.nwg * c.wg_bytes;
+  c.ok = c.smem <= budget && 4 * nb <= 512;
+  return c;
 }
 
 // TC programs: maxdims_host = (slots, steps, edge entries) maxima over the
@@ -1445,24 +1504,16 @@ int launch_tile(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, co
 // for small launches) with as many warpgroups as shared memory allows.
 int launch_tc(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, const float* in, int64_t in_gstride,
               int64_t P, int B, int I, int O, const int32_t* maxdims_host, float* out, int64_t out_gstride,
-              int max_wg, cudaStream_t st) {
+              int max_wg, cudaStream_t st, const int32_t* count_dev = nullptr) {
   if (I > TC_K || (I & 3) || (((uintptr_t)in) & 15)) return -8;
   const int ms = max(maxdims_host[1], 1), me = maxdims_host[2];
   const int nb = tc_rows(ms);
   if (4 * nb > 512) return -8;
-  const uint32_t wg_bytes = tc_wg_bytes(nb);
-  const uint32_t gbuf = (uint32_t)align_up(tc_block(ms, ms, me).bytes + 64, 128);  // + look-ahead slack
-  const int64_t budget = 227 * 1024, ctl = (int64_t)align_up(sizeof(TcShared), 16);
-  auto fit = [&](int nbuf) {
-    int w = max_wg > 0 ? min(max_wg, TC_MAX_WG) : TC_MAX_WG;
-    while (w > 1 && ctl + nbuf * (int64_t)gbuf + (int64_t)w * wg_bytes > budget) --w;
-    return w;
-  };
-  // double-buffered genome blocks unless a single buffer buys another warpgroup
-  const int nbuf = fit(1) > fit(2) ? 1 : 2;
-  const int nwg = fit(nbuf);
-  const int64_t smem = ctl + nbuf * (int64_t)gbuf + (int64_t)nwg * wg_bytes;
-  if (smem > budget) return -6;
+  const TcConfig cfg = tc_config(ms, me, max_wg);
+  if (!cfg.ok) return -6;
+  const uint32_t wg_bytes = cfg.wg_bytes, gbuf = cfg.gbuf;
+  const int nbuf = cfg.nbuf, nwg = cfg.nwg;
+  const int64_t smem = cfg.smem;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1480,10 +1531,98 @@ int launch_tc(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, cons
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -9;
   cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fwd_tc_kernel<<<(unsigned)grid, TC_NT * nwg, smem, st>>>(tmap, prog, L, ids, P, in, in_gstride, B, I, O, nwg,
+  if (grid == 0) return 0;
+  fwd_tc_kernel<<<(unsigned)grid, TC_NT * nwg, smem, st>>>(tmap, prog, L, ids, count_dev, P, in, in_gstride, B, I, O, nwg,
                                                            wg_bytes, gbuf, nbuf, nb, out, out_gstride);
   TNEAT_CHECK_LAUNCH();
   return 0;
+}
+
+// ---------------------------------------------------------------------------
+// device-side launch plan of an FMT_TC population (no host read-back)
+// ---------------------------------------------------------------------------
+// Class of a genome: 0..3 tensor-core programs by MMA width (round16(steps) <=
+// 32, 48, 64, 128) whose hidden-edge entries fit the class buffer; 4 tensor-core
+// programs with more entries (buffer sized by the capacity); 5 standard
+// programs (the tile kernel with capacity-sized shared memory).  One CTA, a
+// deterministic block scan per class: ids[c * P + i] = i-th genome of class c
+// in population order, counts[c].
+constexpr int TC_NCLASS = 6;
+constexpr int TC_CLASS_EDGES = 512;
+__host__ __device__ inline int tc_class_nb(int c) { return c == 0 ? 32 : c == 1 ? 48 : c == 2 ? 64 : 128; }
+
+__global__ void __launch_bounds__(1024, 1) plan_tc_kernel(const uint8_t* __restrict__ prog, int64_t stride, int64_t P,
+                                                          int32_t* __restrict__ ids, int32_t* __restrict__ counts) {
+  __shared__ int wcount[32][TC_NCLASS];
+  __shared__ int base[TC_NCLASS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < TC_NCLASS) base[tid] = 0;
+  __syncthreads();
+  for (int64_t chunk = 0; chunk < P; chunk += 1024) {
+    const int64_t g = chunk + tid;
+    int cls = -1;
+    if (g < P) {
+      const ProgHeader h = *reinterpret_cast<const ProgHeader*>(prog + g * stride);
+      if (h.mode != MODE_TC) {
+        cls = 5;
+      } else {
+        const int nb = tc_rows(h.n_steps);
+        cls = h.n_edges > TC_CLASS_EDGES ? 4 : nb <= 32 ? 0 : nb <= 48 ? 1 : nb <= 64 ? 2 : 3;
+      }
+    }
+    int wpos[TC_NCLASS];
+#pragma unroll
+    for (int c = 0; c < TC_NCLASS; ++c) {
+      const unsigned m = __ballot_sync(0xffffffffu, cls == c);
+      wpos[c] = __popc(m & ((1u << lane) - 1));
+      if (lane == 0) wcount[warp][c] = __popc(m);
+    }
+    __syncthreads();
+    if (tid < TC_NCLASS) {  // exclusive scan over the warps, per class
+      int run = base[tid];
+      for (int w = 0; w < 32; ++w) {
+        const int t = wcount[w][tid];
+        wcount[w][tid] = run;
+        run += t;
+      }
+      base[tid] = run;
+    }
+    __syncthreads();
+    if (cls >= 0) ids[(int64_t)cls * P + wcount[warp][cls] + wpos[cls]] = (int32_t)g;
+    __syncthreads();
+  }
+  if (tid < TC_NCLASS) counts[tid] = base[tid];
+}
+
+// forward of a whole FMT_TC population from the device plan: the plan kernel,
+// then one persistent launch per tensor-core class and a grid-striding tile
+// launch for standard programs, every launch sized from class bounds (no
+// host-side counts or extents)
+int launch_planned(const uint8_t* prog, const ProgLayout& L, int N, int C, int32_t* ids, int32_t* counts,
+                   const float* in, int64_t in_gstride, int64_t P, int B, int I, int O, float* out,
+                   int64_t out_gstride, cudaStream_t st) {
+  const int steps_cap = N < 128 ? N : 128;
+  {  // every class launch must fit before anything is enqueued (-6: the caller
+     // plans on the host instead -- very large genome capacities)
+    if (!tc_config(steps_cap, (int)edge_capacity(N, C), 0).ok) return -6;
+    const int64_t tile_smem = align_up(32ll * N + 8ll * edge_capacity(N, C) + 16, 16) + (int64_t)(N + 2) * 130 * 4;
+    if (tile_smem > 227 * 1024) return -6;
+  }
+  plan_tc_kernel<<<1, 1024, 0, st>>>(prog, L.stride, P, ids, counts);
+  TNEAT_CHECK_LAUNCH();
+  for (int c = 0; c < 5; ++c) {
+    const int nb = c < 4 ? tc_class_nb(c) : tc_rows(steps_cap);
+    if (c < 4 && nb > tc_rows(steps_cap) && c > 0 && tc_class_nb(c - 1) >= tc_rows(steps_cap)) continue;  // empty by construction
+    const int32_t md[3] = {nb + 1, nb, c < 4 ? TC_CLASS_EDGES : (int)edge_capacity(N, C)};
+    const int r = launch_tc(prog, L, ids + (int64_t)c * P, in, in_gstride, P, B, I, O, md, out, out_gstride, 0, st,
+                            counts + c);
+    if (r) return r;
+  }
+  // standard programs (genomes the tensor-core format cannot take, cyclic or
+  // invalid genomes): capacity-sized tile launch
+  const int32_t md[3] = {N + 2, N, (int)edge_capacity(N, C)};
+  return launch_tile<float, 2, 64>(prog, L, ids + 5 * P, in, in_gstride, P, B, I, O, md, out, out_gstride, 4, st,
+                                   counts + 5);
 }
 
 }  // namespace tneat
@@ -1546,6 +1685,34 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
     case 6: return launch_tile<float, 4, 32>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
     default: return launch_tile<float, 1, 128>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
   }
+}
+
+// FMT_TC populations: forward from a device-side launch plan (no host-known
+// launch sizes; see include/tneat.h).  plan_ids: int32[6 * P] and
+// plan_counts: int32[6] scratch owned by the caller.
+int an_forward_planned(const void* program, int64_t program_stride, int N, int C, int precision, int32_t* plan_ids,
+                       int32_t* plan_counts, const void* inputs, int64_t input_genome_stride, int64_t P, int B, int I,
+                       int O, void* outputs, void* stream) {
+  if (P < 0 || B < 0 || I < 1 || O < 1) return -1;
+  if (!(precision & FMT_TC) || (precision & FMT_F64)) return -7;
+  if (P == 0 || B == 0) return 0;
+  if (!program || !inputs || !outputs || !plan_ids || !plan_counts) return -2;
+  if (P > 0x7FFFFFFF / TC_NCLASS) return -5;
+  const ProgLayout L = prog_layout(N, C, O, precision);
+  if (L.stride != program_stride) return -3;
+  return launch_planned((const uint8_t*)program, L, N, C, plan_ids, plan_counts, (const float*)inputs,
+                        input_genome_stride, P, B, I, O, (float*)outputs, (int64_t)B * O, (cudaStream_t)stream);
+}
+
+int an_plan_tc(const void* program, int64_t program_stride, int64_t P, int32_t* plan_ids, int32_t* plan_counts,
+               void* stream) {
+  if (P < 0) return -1;
+  if (!program || !plan_ids || !plan_counts) return -2;
+  if (P > 0x7FFFFFFF / TC_NCLASS) return -5;
+  plan_tc_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>((const uint8_t*)program, program_stride, P, plan_ids,
+                                                         plan_counts);
+  TNEAT_CHECK_LAUNCH();
+  return 0;
 }
 
 // Fused forward + fitness for the built-in problems (problems.py:221-254):

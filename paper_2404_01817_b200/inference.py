@@ -420,8 +420,36 @@ def _bucket_plan(stacked: StackedNetworks, variant: int, subset: np.ndarray | No
     return plan
 
 
+TC_NCLASS = 6  # device launch-plan classes (csrc/forward.cu plan_tc_kernel)
+
+
+def _tc_plan_buffers(stacked: StackedNetworks, device) -> tuple[torch.Tensor, torch.Tensor]:
+    """Scratch of the device-side launch plan (ids int32[6P], counts int32[6]),
+    allocated once per StackedNetworks; the plan itself is rebuilt on the
+    device by every forward (no host read-back)."""
+    bufs = stacked._cache.get("tcplan")
+    if bufs is None:
+        bufs = (torch.empty((TC_NCLASS * max(1, stacked.size),), dtype=torch.int32, device=device),
+                torch.empty((TC_NCLASS,), dtype=torch.int32, device=device))
+        stacked._cache["tcplan"] = bufs
+    return bufs
+
+
+def tc_plan_counts(stacked: StackedNetworks) -> np.ndarray:
+    """Genomes per device-plan class of an FMT_TC population (classes 0-3:
+    tensor-core programs by MMA width 32/48/64/128, 4: tensor-core programs
+    with more hidden-edge entries than the class buffer, 5: standard programs).
+    Diagnostics and tests; the forward does not need it."""
+    ids, counts = _tc_plan_buffers(stacked, stacked.program.device)
+    _native.call("an_plan_tc", ptr(stacked.program), stacked.stride, stacked.size, ptr(ids), ptr(counts),
+                 stream_handle())
+    return counts.cpu().numpy()
+
+
 def _tc_plan(stacked: StackedNetworks) -> tuple[list, list]:
-    """Launch plan of an FMT_TC population: tensor-core programs bucketed by
+    """Host launch plan of an FMT_TC population (the fallback when the device
+    plan's capacity-sized classes do not fit shared memory -- very large
+    genome capacities): tensor-core programs bucketed by
     their MMA width (steps rounded up to 16: it sets the TMEM columns and the
     shared-memory footprint, i.e. the resident CTAs per SM), each bucket sized
     by its own (steps, edge entries) extents; standard programs (genomes the
@@ -464,9 +492,12 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
                    *, shared: bool = False, variant: int = 0, bucketed: bool = True,
                    stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """Device-resident forward: inputs (P,B,I) (or (B,I) with shared=True) on
-    the GPU in the program's dtype -> outputs (P,B,O).  No host syncs after
-    the first call on a given StackedNetworks (the bucket plan is cached)."""
-    ensure_finalized(stacked)
+    the GPU in the program's dtype -> outputs (P,B,O).  Tensor-core (FMT_TC)
+    programs plan their launches on the device (no host sync at all, a
+    transform with sync=False need not be finalized); standard programs use
+    the host bucket plan (cached after the first call)."""
+    if not stacked.precision & FMT_TC:
+        ensure_finalized(stacked)
     dt = _TORCH_DT[stacked.precision]
     if inputs.dtype != dt or not inputs.is_cuda or not inputs.is_contiguous():
         raise ValueError(f"inputs must be a contiguous CUDA {dt} tensor")
@@ -493,9 +524,23 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
             # standard-only kernels (or an unbucketed launch): standard programs
             return forward_device(standard_programs(stacked), inputs, out, shared=shared, variant=variant,
                                   bucketed=bucketed, stream=stream)
-        plan_tc, plan_std = _tc_plan(stacked)
         launch = stream or torch.cuda.current_stream()
         args = (ptr(stacked.program), stacked.stride, stacked.max_nodes, stacked.max_conns, stacked.precision)
+        if not stacked._cache.get("tc_host_plan"):
+            # device-side launch plan: classes and counts never leave the GPU, so a
+            # transform + forward step needs no host synchronisation
+            ids, counts = _tc_plan_buffers(stacked, inputs.device)
+            if launch != torch.cuda.current_stream():
+                ids.record_stream(launch)
+                counts.record_stream(launch)
+            ret = _native.lib().an_forward_planned(*args, ptr(ids), ptr(counts), ptr(inputs), gstride, pop, b, i,
+                                                   stacked.num_outputs, ptr(out), stream_handle(stream))
+            if ret != -6:
+                _native.check("an_forward_planned", ret)
+                return out
+            stacked._cache["tc_host_plan"] = True  # capacity-sized classes do not fit shared memory
+        ensure_finalized(stacked)
+        plan_tc, plan_std = _tc_plan(stacked)
         tpc = variant & 0xFF00
         for key, plan, vv in ((("plan", V_TC), plan_tc, V_TC), (("plan_tcstd", 5), plan_std, 5)):
             if not plan:

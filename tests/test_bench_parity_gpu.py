@@ -1,8 +1,9 @@
 """Parity of the exact benchmarked launch (bench.py's step, BASELINE configs[1]).
 
 The bench transforms the §8d population (pop 10,000, 128/512, I=32, O=8,
-seed 20261018, tanh/sum) and runs the bucketed tensor-core forward
-(fwd_tc_kernel, one launch per MMA-width class) over 4096 inputs per genome
+seed 20261018, tanh/sum) and runs the tensor-core forward from its
+device-side launch plan (fwd_tc_kernel, one persistent launch per MMA-width
+class) over 4096 inputs per genome
 generated on the device (seed 20261019).  This test makes the same calls,
 checks every genome takes the tensor-core format and the plan forms the
 buckets the bench launches, and
@@ -46,17 +47,18 @@ def bench_run():
 
 
 def _plan(tn, st):
-    plan_tc, plan_std = st._cache[("plan", tn.inference.V_TC)]
-    return plan_tc, plan_std
+    """Device launch plan of the benchmarked population: per class, its program rows."""
+    counts = tn.inference.tc_plan_counts(st)
+    ids = st._cache["tcplan"][0].view(tn.inference.TC_NCLASS, -1).cpu().numpy()
+    return [(ids[c, :counts[c]], c) for c in range(tn.inference.TC_NCLASS) if counts[c]], counts
 
 
 def test_bench_plan_has_every_bucket(bench_run):
     tn, st, *_ = bench_run
-    plan, plan_std = _plan(tn, st)
-    assert not plan_std  # every tanh/sum genome takes the tensor-core format
-    sizes = [int(ids.numel()) for ids, _ in plan]
-    assert sum(sizes) == POP
-    assert len(plan) >= 4, sizes  # MMA-width classes of 16 steps: 16..80
+    plan, counts = _plan(tn, st)
+    assert counts[5] == 0  # every tanh/sum genome takes the tensor-core format
+    assert counts.sum() == POP
+    assert (counts[:3] > 0).all(), counts  # MMA-width classes 32 / 48 / 64 are all launched
 
 
 def test_bench_launch_matches_oracle_on_stratified_subset(bench_run):
@@ -67,7 +69,6 @@ def test_bench_launch_matches_oracle_on_stratified_subset(bench_run):
     per = -(-256 // len(plan))
     picks = []
     for ids, _ in plan:
-        ids = ids.cpu().numpy()
         picks += rng.choice(ids, size=min(per, ids.size), replace=False).tolist()
     picks = np.array(sorted(picks[:256] if len(picks) > 256 else picks))
     xs = x[picks].cpu().numpy().astype(np.float64)

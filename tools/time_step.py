@@ -34,8 +34,7 @@ for rep in range(a.reps):
     tn.finalize_transform(st)
     t2 = time.perf_counter()
     if st.precision & tn.inference.FMT_TC:
-        pt, ps = tn.inference._tc_plan(st)
-        plan = pt + ps
+        plan = [c for c in tn.inference.tc_plan_counts(st) if c]
     else:
         plan = tn.inference._bucket_plan(st, (a.variant & 0xF) or 5)
     torch.cuda.synchronize()
