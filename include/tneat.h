@@ -96,11 +96,14 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
  * (a transform + forward step can be enqueued ahead or graph-captured).
  * Replaces inference.forward_arrays (inference.py:185-262) for such
  * populations.  plan_ids int32[6 * P] and plan_counts int32[6] are DEVICE
- * scratch owned by the caller; inputs / outputs as an_forward (float32). */
+ * scratch owned by the caller; inputs / outputs as an_forward (float32).
+ * genome_sq: optional (P,) float32, zeroed by the caller: += the sum of the
+ * genome's squared outputs (a fused fitness epilogue; float atomics, so the
+ * summation order -- and the last bits -- vary between runs), or NULL. */
 int an_forward_planned(const void* program, int64_t program_stride, int N, int C, int precision,
                        int32_t* plan_ids, int32_t* plan_counts, const void* inputs,
                        int64_t input_genome_stride, int64_t P, int B, int I, int O, void* outputs,
-                       void* stream);
+                       float* genome_sq, void* stream);
 
 /* The plan step of an_forward_planned alone (diagnostics): plan_counts[c] =
  * genomes of class c (0..3 tensor-core programs with round16(steps) <= 32, 48,

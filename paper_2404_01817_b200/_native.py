@@ -21,7 +21,7 @@ SIGNATURES: dict[str, tuple] = {
     "an_program_stride": (I64, [I32, I32, I32, I32]),
     "an_transform": (I32, [P, P, I64, I32, I32, I32, I32, I32, I32, I32, P, I64, P, P, P, P, P, P]),
     "an_forward": (I32, [P, I64, I32, I32, I32, P, P, P, I64, I64, I32, I32, I32, P, I32, P]),
-    "an_forward_planned": (I32, [P, I64, I32, I32, I32, P, P, P, I64, I64, I32, I32, I32, P, P]),
+    "an_forward_planned": (I32, [P, I64, I32, I32, I32, P, P, P, I64, I64, I32, I32, I32, P, P, P]),
     "an_plan_tc": (I32, [P, I64, I64, P, P, P]),
     "an_forward_fitness": (I32, [P, I64, I32, I32, I32, P, P, I64, I64, I32, I32, I32, I32, P, P, P]),
     "an_cartpole": (I32, [P, I64, I32, I32, I32, P, I64, P, I32, P, P]),

@@ -470,7 +470,7 @@ template <typename T, int S, int NT>
 __device__ __forceinline__ void tile_task(const uint8_t* __restrict__ prog, const ProgLayout& L,
                                           const int32_t* __restrict__ genome_ids, const T* __restrict__ in,
                                           int64_t in_gstride, int B, int I, int O, int64_t task, int run, int tpc,
-                                          T* __restrict__ out, int64_t out_gstride) {
+                                          T* __restrict__ out, int64_t out_gstride, float* __restrict__ gsq) {
   constexpr int TT = NT * S;
   constexpr int RB = (TT + S) * sizeof(T);  // bytes of one value slot row (padded by S)
   using PackT = Pack<T, S>;
@@ -553,6 +553,7 @@ __device__ __forceinline__ void tile_task(const uint8_t* __restrict__ prog, cons
     base_[2 * (RB / 4)] = (x_).z;                   \
     base_[3 * (RB / 4)] = (x_).w;                   \
   }
+  float sq = 0.0f;  // fused fitness: sum of squared outputs of this thread's samples
   for (int tile = run * tpc; tile < tile_end; ++tile) {
     const int t0 = tile * TT;
     const int nt = min(TT, B - t0);
@@ -662,6 +663,9 @@ __device__ __forceinline__ void tile_task(const uint8_t* __restrict__ prog, cons
         float4* row = reinterpret_cast<float4*>(go + (int64_t)(s0 + j) * 8);
         row[0] = make_float4(v[0].v[j], v[1].v[j], v[2].v[j], v[3].v[j]);
         row[1] = make_float4(v[4].v[j], v[5].v[j], v[6].v[j], v[7].v[j]);
+        if (gsq)
+#pragma unroll
+          for (int o = 0; o < 8; ++o) sq += (float)(v[o].v[j] * v[o].v[j]);
       }
     } else {
 #pragma unroll
@@ -671,10 +675,17 @@ __device__ __forceinline__ void tile_task(const uint8_t* __restrict__ prog, cons
         T* row = go + (int64_t)s * O;
         for (int o = 0; o < O; ++o) {
           const uint16_t sl = __ldg(os + o);
-          row[o] = sl != NO_SLOT ? *reinterpret_cast<const T*>(vb + sl * RB + j * sizeof(T)) : T(NAN);
+          const T y = sl != NO_SLOT ? *reinterpret_cast<const T*>(vb + sl * RB + j * sizeof(T)) : T(NAN);
+          row[o] = y;
+          sq += (float)(y * y);
         }
       }
     }
+  }
+  if (gsq) {  // fused fitness (device-planned forward): one atomic per warp and task
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, d);
+    if ((tid & 31) == 0) atomicAdd(gsq + gi, sq);
   }
 }
 
@@ -687,11 +698,12 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
                                                       const int32_t* __restrict__ count_dev,
                                                       const T* __restrict__ in, int64_t in_gstride,
                                                       int B, int I, int O, int runs, int tpc,
-                                                      T* __restrict__ out, int64_t out_gstride) {
+                                                      T* __restrict__ out, int64_t out_gstride,
+                                                      float* __restrict__ gsq) {
   if (!count_dev) {
     const int64_t task = blockIdx.x / runs;
     tile_task<T, S, NT>(prog, L, genome_ids, in, in_gstride, B, I, O, task, (int)(blockIdx.x - task * runs), tpc,
-                        out, out_gstride);
+                        out, out_gstride, gsq);
     return;
   }
   const int64_t n = (int64_t)__ldg(count_dev) * runs;
@@ -699,7 +711,7 @@ __global__ void __launch_bounds__(NT, TNEAT_TILE_MINB(NT)) fwd_tile_kernel(const
     if (t != blockIdx.x) __syncthreads();  // the previous task's shared memory is consumed
     const int64_t task = t / runs;
     tile_task<T, S, NT>(prog, L, genome_ids, in, in_gstride, B, I, O, task, (int)(t - task * runs), tpc, out,
-                        out_gstride);
+                        out_gstride, gsq);
   }
 }
 
@@ -899,7 +911,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
               const int32_t* __restrict__ genome_ids, const int32_t* __restrict__ count_dev, int64_t P,
               const float* __restrict__ in, int64_t in_gstride,
               int B, int I, int O, int nwg, uint32_t wg_bytes, uint32_t gbuf_bytes, int nbuf, int nb_max,
-              float* __restrict__ out,
+              float* __restrict__ gsq, float* __restrict__ out,
               int64_t out_gstride) {
   // no static shared memory: the dynamic area starts the CTA's shared window,
   // 1024-aligned for the swizzled TMA tiles; the control block is at its end
@@ -988,6 +1000,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
     const uint16_t* isrc = reinterpret_cast<const uint16_t*>(gp + L.off_isrc);
     const float* iw = reinterpret_cast<const float*>(gp + L.off_iw);
 
+    float sq = 0.0f;  // fused fitness: sum of squared outputs of this thread's samples
     if (n_steps > 0 && wt == 0 && wg < tiles) {  // this warpgroup's first tile
       mbar_expect_tx(bar_tma, TC_IN_BYTES);
       tma_load_3d(in_addr, &tmap_in, 0, wg * TC_TT, zc, bar_tma);
@@ -1136,6 +1149,11 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
           row[0] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
           row[1] = make_float4(v[4].y, v[5].y, v[6].y, v[7].y);
         }
+        if (gsq) {
+          const float m0 = s0 < B ? 1.0f : 0.0f, m1 = s1 < B ? 1.0f : 0.0f;
+#pragma unroll
+          for (int o = 0; o < 8; ++o) sq = fmaf(m0 * v[o].x, v[o].x, fmaf(m1 * v[o].y, v[o].y, sq));
+        }
       } else {
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
@@ -1145,7 +1163,9 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
           const uint16_t* os = reinterpret_cast<const uint16_t*>(gp + L.off_out);
           for (int o = 0; o < O; ++o) {
             const uint16_t sl = __ldg(os + o);
-            row[o] = sl != NO_SLOT ? reinterpret_cast<const float*>(vb + (uint32_t)sl * TC_RB)[h] : NAN;
+            const float y = sl != NO_SLOT ? reinterpret_cast<const float*>(vb + (uint32_t)sl * TC_RB)[h] : NAN;
+            row[o] = y;
+            sq = fmaf(y, y, sq);
           }
         }
       }
@@ -1157,6 +1177,11 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
         tma_load_3d(in_addr, &tmap_in, 0, next * TC_TT, zc, bar_tma);
       }
 #endif
+    }
+    if (gsq && n_steps > 0) {  // one atomic per warp and genome
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, d);
+      if ((tid & 31) == 0) atomicAdd(gsq + gi, sq);
     }
     __syncthreads();  // every warpgroup is done with buffer `buf` before it is restaged
     if (nbuf == 1 && tid == 0 && task + gridDim.x < P) issue_stage(task + gridDim.x, 0);
@@ -1445,7 +1470,7 @@ int launch_warp(const uint8_t* prog, const ProgLayout& L, int64_t P, const T* in
 template <typename T, int S, int NT>
 int launch_tile(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, const T* in, int64_t in_gstride,
                 int64_t P, int B, int I, int O, const int32_t* maxdims_host, T* out, int64_t out_gstride,
-                int tpc, cudaStream_t st, const int32_t* count_dev = nullptr) {
+                int tpc, cudaStream_t st, const int32_t* count_dev = nullptr, float* gsq = nullptr) {
   constexpr int TT = NT * S;
   const int tiles = (B + TT - 1) / TT;
   tpc = max(1, min(tpc, tiles));
@@ -1466,7 +1491,7 @@ int launch_tile(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, co
   if (smem > 227 * 1024) return -6;
   cudaFuncSetAttribute(fwd_tile_kernel<T, S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fwd_tile_kernel<T, S, NT><<<(unsigned)grid, NT, smem, st>>>(prog, L, ids, count_dev, in, in_gstride, B, I, O, runs, tpc,
-                                                              out, out_gstride);
+                                                              out, out_gstride, gsq);
   TNEAT_CHECK_LAUNCH();
   return 0;
 }
@@ -1504,7 +1529,7 @@ inline TcConfig tc_config(int ms, int me, int max_wg) {
 // for small launches) with as many warpgroups as shared memory allows.
 int launch_tc(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, const float* in, int64_t in_gstride,
               int64_t P, int B, int I, int O, const int32_t* maxdims_host, float* out, int64_t out_gstride,
-              int max_wg, cudaStream_t st, const int32_t* count_dev = nullptr) {
+              int max_wg, cudaStream_t st, const int32_t* count_dev = nullptr, float* gsq = nullptr) {
   if (I > TC_K || (I & 3) || (((uintptr_t)in) & 15)) return -8;
   const int ms = max(maxdims_host[1], 1), me = maxdims_host[2];
   const int nb = tc_rows(ms);
@@ -1533,7 +1558,7 @@ int launch_tc(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, cons
   cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (grid == 0) return 0;
   fwd_tc_kernel<<<(unsigned)grid, TC_NT * nwg, smem, st>>>(tmap, prog, L, ids, count_dev, P, in, in_gstride, B, I, O, nwg,
-                                                           wg_bytes, gbuf, nbuf, nb, out, out_gstride);
+                                                           wg_bytes, gbuf, nbuf, nb, gsq, out, out_gstride);
   TNEAT_CHECK_LAUNCH();
   return 0;
 }
@@ -1600,7 +1625,7 @@ __global__ void __launch_bounds__(1024, 1) plan_tc_kernel(const uint8_t* __restr
 // host-side counts or extents)
 int launch_planned(const uint8_t* prog, const ProgLayout& L, int N, int C, int32_t* ids, int32_t* counts,
                    const float* in, int64_t in_gstride, int64_t P, int B, int I, int O, float* out,
-                   int64_t out_gstride, cudaStream_t st) {
+                   int64_t out_gstride, float* gsq, cudaStream_t st) {
   const int steps_cap = N < 128 ? N : 128;
   {  // every class launch must fit before anything is enqueued (-6: the caller
      // plans on the host instead -- very large genome capacities)
@@ -1615,14 +1640,14 @@ int launch_planned(const uint8_t* prog, const ProgLayout& L, int N, int C, int32
     if (c < 4 && nb > tc_rows(steps_cap) && c > 0 && tc_class_nb(c - 1) >= tc_rows(steps_cap)) continue;  // empty by construction
     const int32_t md[3] = {nb + 1, nb, c < 4 ? TC_CLASS_EDGES : (int)edge_capacity(N, C)};
     const int r = launch_tc(prog, L, ids + (int64_t)c * P, in, in_gstride, P, B, I, O, md, out, out_gstride, 0, st,
-                            counts + c);
+                            counts + c, gsq);
     if (r) return r;
   }
   // standard programs (genomes the tensor-core format cannot take, cyclic or
   // invalid genomes): capacity-sized tile launch
   const int32_t md[3] = {N + 2, N, (int)edge_capacity(N, C)};
   return launch_tile<float, 2, 64>(prog, L, ids + 5 * P, in, in_gstride, P, B, I, O, md, out, out_gstride, 4, st,
-                                   counts + 5);
+                                   counts + 5, gsq);
 }
 
 }  // namespace tneat
@@ -1692,7 +1717,7 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
 // plan_counts: int32[6] scratch owned by the caller.
 int an_forward_planned(const void* program, int64_t program_stride, int N, int C, int precision, int32_t* plan_ids,
                        int32_t* plan_counts, const void* inputs, int64_t input_genome_stride, int64_t P, int B, int I,
-                       int O, void* outputs, void* stream) {
+                       int O, void* outputs, float* genome_sq, void* stream) {
   if (P < 0 || B < 0 || I < 1 || O < 1) return -1;
   if (!(precision & FMT_TC) || (precision & FMT_F64)) return -7;
   if (P == 0 || B == 0) return 0;
@@ -1701,7 +1726,8 @@ int an_forward_planned(const void* program, int64_t program_stride, int N, int C
   const ProgLayout L = prog_layout(N, C, O, precision);
   if (L.stride != program_stride) return -3;
   return launch_planned((const uint8_t*)program, L, N, C, plan_ids, plan_counts, (const float*)inputs,
-                        input_genome_stride, P, B, I, O, (float*)outputs, (int64_t)B * O, (cudaStream_t)stream);
+                        input_genome_stride, P, B, I, O, (float*)outputs, (int64_t)B * O, genome_sq,
+                        (cudaStream_t)stream);
 }
 
 int an_plan_tc(const void* program, int64_t program_stride, int64_t P, int32_t* plan_ids, int32_t* plan_counts,

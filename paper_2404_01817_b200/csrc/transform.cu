@@ -322,6 +322,11 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     s.skey[r] = packed;
   }
   n_live = __reduce_add_sync(0xffffffffu, n_live);
+  // io fast path (search.py:112-114): io keys 0..I+O-1 at rows 0..I+O-1 resolve
+  // without a search (the sorted table gives the same rows)
+  bool io_fast = true;
+  for (int r = lane; r < io; r += 32) io_fast = io_fast && gn[(int64_t)r * 5] == (double)r;
+  io_fast = __all_sync(0xffffffffu, io_fast);
   __syncwarp();
   warp_bitonic_sort(s.skey, Npad);
 
@@ -338,8 +343,8 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
         if (!key_ok(ik) || !key_ok(ok)) {
           status |= ST_BAD_KEY;
         } else {
-          sr = lookup_row(s.skey, Npad, (uint64_t)ik);
-          dr = lookup_row(s.skey, Npad, (uint64_t)ok);
+          sr = (io_fast && ik < (double)io) ? (int)ik : lookup_row(s.skey, Npad, (uint64_t)ik);
+          dr = (io_fast && ok < (double)io) ? (int)ok : lookup_row(s.skey, Npad, (uint64_t)ok);
           if (sr < 0 || dr < 0) status |= ST_DANGLING;
           else en = gc[(int64_t)c * 4 + 2] == 1.0;
         }
@@ -607,8 +612,10 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
         }
         if (mw != 0.0 && (mw < 0x1p-62 || mw >= 0x1p63)) bad = 1;
         // the kernel folds the column factor cf = 2^(e - 12) into the step: hidden
-        // weights / cf and response * cf must stay normal floats
+        // weights / cf and response * cf must stay normal floats (the exponent is
+        // kept in su_start, free for TC programs from here on)
         const int ewx = mw != 0.0 ? ilogb(mw) : 12;
+        s.su_start[r] = ewx;
         const double up = ldexp(1.0, 12 - ewx), dn = ldexp(1.0, ewx - 12);
         for (int e = s.in_start[r]; e < s.in_start[r + 1]; ++e) {
           const typename KT::E kk = s.ekey[e];
@@ -842,12 +849,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       // cf = 2^(e - 12) (the MMA epilogue then skips one multiply per step), so
       // the response carries cf; tanh groups also pre-scale by -2 log2(e)
       // (common.cuh GroupTC).  Powers of two: bit-identical results.
-      double mw = 0.0;
-      for (int e = e0; e < e0 + cnt; ++e) {
-        const typename KT::E kk = s.ekey[e];
-        if (s.flags[KT::src(kk)] & F_INPUT) mw = fmax(mw, fabs(gc[KT::row(kk) * 4 + 3]));
-      }
-      const double cfk = ldexp(1.0, (mw != 0.0 ? ilogb(mw) : 12) - 12);
+      const double cfk = ldexp(1.0, s.su_start[row] - 12);
       const double kk = (gr.cls & GRP_TANH_SUM) ? (double)TANH_K : 1.0;
       st.bias = (T)(nr[1] * kk);
       st.resp = (T)(nr[2] * cfk * kk);
@@ -875,12 +877,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
         uint16_t* isrc = (uint16_t*)(gp + L.off_isrc);
         float* iw = (float*)(gp + L.off_iw);
         uint8_t* brow = blk + tb.b;
-        double mw = 0.0;
-        for (int e = e0; e < e0 + cnt; ++e) {
-          const typename KT::E kk = s.ekey[e];
-          if (s.flags[KT::src(kk)] & F_INPUT) mw = fmax(mw, fabs(gc[KT::row(kk) * 4 + 3]));
-        }
-        const int ewx = mw != 0.0 ? ilogb(mw) : 12;
+        const int ewx = s.su_start[row];
         const double sc = ldexp(1.0, 27 - ewx), up = ldexp(1.0, 12 - ewx);
         ((float*)(blk + tb.cf))[k] = pow2f(12 - ewx);  // 1 / cf (the exact path's partials)
 #pragma unroll 1

@@ -490,12 +490,17 @@ def standard_programs(stacked: StackedNetworks) -> StackedNetworks:
 
 def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Tensor | None = None,
                    *, shared: bool = False, variant: int = 0, bucketed: bool = True,
-                   stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+                   stream: torch.cuda.Stream | None = None,
+                   sq_sum: torch.Tensor | None = None) -> torch.Tensor:
     """Device-resident forward: inputs (P,B,I) (or (B,I) with shared=True) on
     the GPU in the program's dtype -> outputs (P,B,O).  Tensor-core (FMT_TC)
     programs plan their launches on the device (no host sync at all, a
     transform with sync=False need not be finalized); standard programs use
-    the host bucket plan (cached after the first call)."""
+    the host bucket plan (cached after the first call).
+
+    ``sq_sum``: optional (P,) float32 CUDA tensor, accumulated with each
+    genome's sum of squared outputs by the device-planned forward's fused
+    epilogue (the caller zeroes it); other launch paths reduce ``out``."""
     if not stacked.precision & FMT_TC:
         ensure_finalized(stacked)
     dt = _TORCH_DT[stacked.precision]
@@ -523,9 +528,13 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
         if v not in (0, V_TC) or (v == 0 and b < TC_MIN_BATCH) or not bucketed:
             # standard-only kernels (or an unbucketed launch): standard programs
             return forward_device(standard_programs(stacked), inputs, out, shared=shared, variant=variant,
-                                  bucketed=bucketed, stream=stream)
+                                  bucketed=bucketed, stream=stream, sq_sum=sq_sum)
         launch = stream or torch.cuda.current_stream()
         args = (ptr(stacked.program), stacked.stride, stacked.max_nodes, stacked.max_conns, stacked.precision)
+        if "tc_host_plan" not in stacked._cache and "modes" in stacked._cache:
+            # finalized populations that are mostly standard programs (mixed
+            # aggregations) keep the tile kernel's tight per-bucket launches
+            stacked._cache["tc_host_plan"] = bool((stacked._cache["modes"] != MODE_TC).mean() > 0.5)
         if not stacked._cache.get("tc_host_plan"):
             # device-side launch plan: classes and counts never leave the GPU, so a
             # transform + forward step needs no host synchronisation
@@ -534,7 +543,9 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
                 ids.record_stream(launch)
                 counts.record_stream(launch)
             ret = _native.lib().an_forward_planned(*args, ptr(ids), ptr(counts), ptr(inputs), gstride, pop, b, i,
-                                                   stacked.num_outputs, ptr(out), stream_handle(stream))
+                                                   stacked.num_outputs, ptr(out),
+                                                   ptr(sq_sum) if sq_sum is not None else None,
+                                                   stream_handle(stream))
             if ret != -6:
                 _native.check("an_forward_planned", ret)
                 return out
@@ -552,6 +563,7 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
                 _native.call("an_forward", *args, _maxdims_arg(stacked, md), ptr(ids), ptr(inputs), gstride,
                              int(ids.numel()), b, i, stacked.num_outputs, ptr(out), vv | tpc,
                              stream_handle(stream))
+        _sq_sum_from_out(out, sq_sum, stream)
         return out
     v = (variant & 0xF) or (5 if b >= 192 else (3 if b >= 96 else 8))
     args = (ptr(stacked.program), stacked.stride, stacked.max_nodes, stacked.max_conns, stacked.precision)
@@ -569,7 +581,16 @@ def forward_device(stacked: StackedNetworks, inputs: torch.Tensor, out: torch.Te
                          int(ids.numel()), *tail)
     else:
         _native.call("an_forward", *args, _maxdims_arg(stacked), None, ptr(inputs), gstride, pop, *tail)
+    _sq_sum_from_out(out, sq_sum, stream)
     return out
+
+
+def _sq_sum_from_out(out: torch.Tensor, sq_sum: torch.Tensor | None, stream) -> None:
+    """sq_sum += per-genome sum of squared outputs (paths without the fused epilogue)."""
+    if sq_sum is None:
+        return
+    with torch.cuda.stream(stream or torch.cuda.current_stream()):
+        sq_sum.add_(torch.linalg.vector_norm(out.view(out.shape[0], -1).float(), dim=1).square_())
 
 
 def _maxdims_arg(stacked: StackedNetworks, dims=None) -> int:

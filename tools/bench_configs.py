@@ -71,7 +71,7 @@ def bench_xor(a):
         out["cpu_reference_gen_per_s"] = rg / rdt
         out["cpu_reference_generations_timed"] = rg
         out["speedup_vs_cpu"] = out["gen_per_s"] / out["cpu_reference_gen_per_s"]
-    print(json.dumps(out), flush=True)
+    return out
 
 
 def bench_generation(a):
@@ -107,11 +107,28 @@ def bench_generation(a):
                        "gen_s": t[3] - t[0], "species": len(species)})
     genome_bytes = (cfg.max_nodes * 5 + cfg.max_conns * 4) * 8
     last = phases[-1]
+    ref = None
+    if getattr(a, "ref_pop", 0):
+        # the unmodified reference's evolve_step (runner.py:165-169 loop pattern)
+        # on the same host, one generation at ref_pop genomes, 1 thread
+        an = _ref_arrayneat()
+        from arrayneat.runner import init_state as ref_init
+        rcfg = an.NeatConfig(seed=0, pop_size=a.ref_pop, inputs=2, outputs=1, problem="xor", max_nodes=50,
+                             max_conns=100, compatibility_threshold=1.0, max_species=10)
+        st = ref_init(rcfg)
+        prob = an.make_problem(rcfg)
+        tt = time.perf_counter()
+        an.evolve_step(st.population, st.species, rcfg, an.RngStream(0).child(0), st.allocator, prob)
+        rdt = time.perf_counter() - tt
+        ref = {"pop": a.ref_pop, "s_per_gen": rdt, "gen_per_s": 1.0 / rdt,
+               "scaled_s_per_gen_at_pop": rdt * a.pop / a.ref_pop, "threads": 1,
+               "note": "generation 0 from init_state; scaled linearly to the GPU run's population"}
     out = {"config": f"3: generation pop {a.pop} 50/100 (XOR, threshold 1.0)", "init_s": t_init,
            "phases": phases, "gen_per_s": 1.0 / last["gen_s"],
            "reproduce_GBps_min_traffic": 3 * a.pop * genome_bytes / last["reproduce_s"] / 1e9,
-           "genome_bytes": genome_bytes, "gpu_mem_GB": torch.cuda.max_memory_allocated() / 1e9}
-    print(json.dumps(out), flush=True)
+           "genome_bytes": genome_bytes, "gpu_mem_GB": torch.cuda.max_memory_allocated() / 1e9,
+           "cpu_reference": ref}
+    return out
 
 
 def bench_hyperneat(a):
@@ -160,7 +177,7 @@ def bench_hyperneat(a):
         dt = (time.perf_counter() - tt) / k
         out["cpu_oracle_s_per_genome"] = dt
         out["cpu_oracle_kind"] = "port (no reference HyperNEAT), 1 thread"
-    print(json.dumps(out), flush=True)
+    return out
 
 
 def bench_recurrent(a):
@@ -204,7 +221,7 @@ def bench_recurrent(a):
         dt = time.perf_counter() - tt
         out["cpu_oracle_genome_steps_per_s_K5"] = 10 / dt
         out["cpu_oracle_kind"] = "port (no reference recurrent path), 1 thread, 10 steps of genome 0"
-    print(json.dumps(out), flush=True)
+    return out
 
 
 def main():
@@ -221,8 +238,9 @@ def main():
                 "recurrent": (10_000, 1)}
     a.pop = a.pop or defaults[a.which][0]
     a.gens = a.gens or defaults[a.which][1]
-    {"xor": bench_xor, "generation": bench_generation, "hyperneat": bench_hyperneat,
-     "recurrent": bench_recurrent}[a.which](a)
+    out = {"xor": bench_xor, "generation": bench_generation, "hyperneat": bench_hyperneat,
+           "recurrent": bench_recurrent}[a.which](a)
+    print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":

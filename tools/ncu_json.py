@@ -30,10 +30,10 @@ def main(rep, out, note=""):
                 except ValueError:
                     pass
         kernels.append(k)
-    fwd = [k for k in kernels if "fwd_" in k["kernel"]]
+    fwd = [k for k in kernels if "fwd_" in k["kernel"] or "plan_tc" in k["kernel"]]
     traffic = sum(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0) for k in fwd)
-    doc = {"source": note, "note": "forward pass = one launch per occupancy bucket; traffic is summed over the "
-                                   "buckets of one pass",
+    doc = {"source": note, "note": "forward pass = every launch of one forward (device plan + class launches, "
+                                   "or one launch per occupancy bucket); traffic is summed over the pass",
            "forward_launches": len(fwd), "forward_time_s_cold": sum(k["gpu__time_duration.sum"] for k in fwd),
            "dram_bytes_per_launch": traffic, "dram_bytes_per_pass": traffic, "kernels": kernels}
     json.dump(doc, open(out, "w"), indent=1)
