@@ -925,9 +925,19 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
   const uint32_t slot_cols = 4u * (uint32_t)nb_max;
   const uint32_t n_slots = 512u / slot_cols;
   const int tiles = (B + TC_TT - 1) / TC_TT;
+  // tasks: (genome, run of tiles).  A genome is one run unless the launch has
+  // fewer genomes than CTAs (small classes): then its tiles are split into up
+  // to gridDim / P runs (each of >= nwg tiles) so every SM gets work
+  int runs = 1;
+  if (P > 0 && P < (int64_t)gridDim.x) {
+    const int64_t want = ((int64_t)gridDim.x + P - 1) / P, cap = tiles / nwg > 1 ? tiles / nwg : 1;
+    runs = (int)(want < cap ? want : cap);
+  }
+  const int run_tiles = (tiles + runs - 1) / runs;
+  const int64_t n_tasks = P * runs;
 
-  auto issue_stage = [&](int64_t task, int buf) {  // one thread: header + block of genome `task`
-    const int64_t gi = genome_ids ? (int64_t)__ldg(genome_ids + task) : task;
+  auto issue_stage = [&](int64_t task, int buf) {  // one thread: header + block of task's genome
+    const int64_t gi = genome_ids ? (int64_t)__ldg(genome_ids + task / runs) : task / runs;
     const uint8_t* gp = prog + gi * L.stride;
     const ProgHeader hdr = *reinterpret_cast<const ProgHeader*>(gp);
     const int ns = hdr.mode == MODE_TC ? hdr.n_steps : 0, ng = hdr.mode == MODE_TC ? hdr.n_groups : 0;
@@ -955,7 +965,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
     sh.tmem_mask = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (blockIdx.x < P) issue_stage(blockIdx.x, 0);
+    if (blockIdx.x < n_tasks) issue_stage(blockIdx.x, 0);
   }
   tc_fence_before();
   __syncthreads();
@@ -969,13 +979,15 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
   uint32_t tphase = 0, mphase = 0, gphase[2] = {0u, 0u};
 
   int k = 0;
-  for (int64_t task = blockIdx.x; task < P; task += gridDim.x, ++k) {
-    // two buffers: the next genome's block is in flight during this one; one
-    // buffer (when a second would cost a warpgroup): staged after the barrier
+  for (int64_t task = blockIdx.x; task < n_tasks; task += gridDim.x, ++k) {
+    // two buffers: the next task's genome block is in flight during this one;
+    // one buffer (when a second would cost a warpgroup): staged after the barrier
     const int buf = nbuf == 2 ? (k & 1) : 0;
     mbar_wait(smem_u32(&sh.gbar[buf]), gphase[buf]);
     gphase[buf] ^= 1u;
-    if (nbuf == 2 && tid == 0 && task + gridDim.x < P) issue_stage(task + gridDim.x, buf ^ 1);
+    if (nbuf == 2 && tid == 0 && task + gridDim.x < n_tasks) issue_stage(task + gridDim.x, buf ^ 1);
+    const int run = (int)(task % runs);
+    const int t_begin = run * run_tiles, t_end = min(tiles, t_begin + run_tiles);
     const int n_steps = sh.hdr[buf][0], n_edges = sh.hdr[buf][1], n_groups = sh.hdr[buf][2];
     const int64_t gi = sh.hdr[buf][3];
     const int nb = tc_rows(n_steps);
@@ -1001,17 +1013,17 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
     const float* iw = reinterpret_cast<const float*>(gp + L.off_iw);
 
     float sq = 0.0f;  // fused fitness: sum of squared outputs of this thread's samples
-    if (n_steps > 0 && wt == 0 && wg < tiles) {  // this warpgroup's first tile
+    if (n_steps > 0 && wt == 0 && t_begin + wg < t_end) {  // this warpgroup's first tile
       mbar_expect_tx(bar_tma, TC_IN_BYTES);
-      tma_load_3d(in_addr, &tmap_in, 0, wg * TC_TT, zc, bar_tma);
+      tma_load_3d(in_addr, &tmap_in, 0, (t_begin + wg) * TC_TT, zc, bar_tma);
     }
-    for (int tile = wg; tile < tiles && n_steps > 0; tile += nwg) {
+    for (int tile = t_begin + wg; tile < t_end && n_steps > 0; tile += nwg) {
       const int s0 = tile * TC_TT + wt, s1 = s0 + TC_NT;  // this thread's samples
       const int next = tile + nwg;
       // ---- 1-2: input rows -> block scales -> digit planes (A rows wt of both halves)
       mbar_wait_sleep(bar_tma, tphase);
       tphase ^= 1u;
-      if (wt == 0 && next < tiles && pf_l2)  // next tile: HBM -> L2 while this one computes
+      if (wt == 0 && next < t_end && pf_l2)  // next tile: HBM -> L2 while this one computes
         prefetch_l2(gin + (int64_t)next * TC_TT * I, (uint32_t)(min(TC_TT, B - next * TC_TT) * I * 4));
       // the input tile sits at the end of the area: A half 0 ([0, 24K)) only
       // overlaps input rows of half 0, so each half is read (into registers),
@@ -1111,7 +1123,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
         }
       }
 #ifdef TNEAT_DIAG_TC_EARLYTMA  // diagnostic builds only (wrong results): next tile's TMA before the sweep
-      if (wt == 0 && next < tiles) {
+      if (wt == 0 && next < t_end) {
         mbar_expect_tx(bar_tma, TC_IN_BYTES);
         tma_load_3d(in_addr, &tmap_in, 0, next * TC_TT, zc, bar_tma);
       }
@@ -1171,7 +1183,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
       }
       named_barrier_sync(bar_id, TC_NT);  // slots dead: the next tile's inputs may land
 #ifndef TNEAT_DIAG_TC_EARLYTMA
-      if (wt == 0 && next < tiles) {
+      if (wt == 0 && next < t_end) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(bar_tma, TC_IN_BYTES);
         tma_load_3d(in_addr, &tmap_in, 0, next * TC_TT, zc, bar_tma);
@@ -1184,7 +1196,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
       if ((tid & 31) == 0) atomicAdd(gsq + gi, sq);
     }
     __syncthreads();  // every warpgroup is done with buffer `buf` before it is restaged
-    if (nbuf == 1 && tid == 0 && task + gridDim.x < P) issue_stage(task + gridDim.x, 0);
+    if (nbuf == 1 && tid == 0 && task + gridDim.x < n_tasks) issue_stage(task + gridDim.x, 0);
   }
   tc_fence_before();
   __syncthreads();

@@ -339,3 +339,44 @@ def test_split_groups_every_kernel(tn, precision, tol):
         out = tn.forward_device(st, torch.from_numpy(x).cuda(), variant=variant).cpu().numpy()
         for p in range(24):
             assert _rel_err(out[p], refs[p]) <= tol, (variant, p)
+
+
+def test_fused_fitness_epilogue_matches_outputs(tn):
+    """The device-planned forward's fused epilogue (sum of each genome's squared
+    outputs, float atomics) equals the sum over the returned outputs; populations
+    that plan on the host reduce the outputs instead -- same contract."""
+    import torch
+    from oracle import arrayneat_oracle as orc
+    for variant, pop in (("T", 300), ("M", 40)):
+        nodes, conns = orc.synthetic_population(pop, 128, 512, 32, 8, seed=90 + pop, variant=variant)
+        st, _ = tn.transform_arrays(nodes, conns, 32, 8, sync=False)
+        x = torch.randn(pop, 777, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(9))
+        sq = torch.zeros(pop, device="cuda")
+        out = tn.forward_device(st, x, sq_sum=sq)
+        ref = out.double().square().sum(dim=(1, 2))
+        torch.testing.assert_close(sq.double(), ref, rtol=2e-6, atol=1e-3)
+
+
+def test_device_plan_classes_cover_population(tn):
+    """The device plan puts every genome in exactly one class, in population
+    order within a class, and the planned forward equals the host-planned one
+    bit for bit (same kernels, same per-genome work)."""
+    import torch
+    from oracle import arrayneat_oracle as orc
+    nodes, conns = orc.synthetic_population(200, 128, 512, 32, 8, seed=93)
+    nm, cm = orc.synthetic_population(30, 128, 512, 32, 8, seed=94, variant="M")
+    nodes, conns = np.concatenate([nodes, nm]), np.concatenate([conns, cm])
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8)
+    counts = tn.inference.tc_plan_counts(st)
+    ids = st._cache["tcplan"][0].view(tn.inference.TC_NCLASS, -1).cpu().numpy()
+    got = np.concatenate([ids[c, :counts[c]] for c in range(tn.inference.TC_NCLASS)])
+    assert np.array_equal(np.sort(got), np.arange(st.size))
+    for c in range(tn.inference.TC_NCLASS):
+        assert np.all(np.diff(ids[c, :counts[c]]) > 0)
+    assert counts[5] == int((st._cache["modes"] != tn.inference.MODE_TC).sum())
+    x = torch.randn(st.size, 600, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(10))
+    st._cache["tc_host_plan"] = False
+    planned = tn.forward_device(st, x)
+    st._cache["tc_host_plan"] = True
+    hosted = tn.forward_device(st, x)
+    assert torch.equal(planned, hosted)
