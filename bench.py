@@ -353,6 +353,25 @@ def secondary(dev) -> dict:
     return out
 
 
+def shard_of(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous equal shard of the population for ``rank`` (strong scaling,
+    SURVEY.md §8e): [lo, lo + total / world)."""
+    if total % world:
+        raise SystemExit(f"pop {total} is not divisible by {world} ranks")
+    shard = total // world
+    return rank * shard, shard
+
+
+def gather_fitness(fit_local, fit_all, world: int) -> None:
+    """The step's one collective: every rank receives the whole (P,) fitness
+    vector (NCCL all-gather over NVLink; gloo in the CPU tests)."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.all_gather_into_tensor(fit_all, fit_local)
+    else:
+        fit_all.copy_(fit_local)
+
+
 def _free_port() -> int:
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
@@ -369,10 +388,7 @@ def run_ours(args, rank: int, world: int) -> None:
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     total = args.pop
-    if total % world:
-        raise SystemExit(f"pop {total} is not divisible by {world} ranks")
-    shard = total // world
-    lo = rank * shard
+    lo, shard = shard_of(total, world, rank)
     # the same 10k population for every world size; rank r owns genomes [lo, lo + shard)
     nodes_all, conns_all = synthetic_population(total, MAXN, MAXC, NIN, NOUT, seed=20261018)
     nodes_h, conns_h = nodes_all[lo:lo + shard].copy(), conns_all[lo:lo + shard].copy()
@@ -428,11 +444,7 @@ def run_ours(args, rank: int, world: int) -> None:
             # each genome's squared outputs (no extra pass over the outputs)
             sq.zero_()
             tn.forward_device(st, x, out, variant=args.variant, stream=fw, sq_sum=sq)
-            fit = sq.mul(-1.0 / (BATCH * NOUT))
-            if world > 1:
-                dist.all_gather_into_tensor(fit_all, fit)
-            else:
-                fit_all.copy_(fit)
+            gather_fitness(sq.mul(-1.0 / (BATCH * NOUT)), fit_all, world)
         live.append(st)
         if len(live) > 2:
             live.pop(0)
