@@ -3,6 +3,7 @@ is bench.py).  One JSON line per measurement; GPU times from CUDA events or
 synchronized wall clock as stated; CPU reference on the same host.
 
     python tools/bench_configs.py xor|generation|hyperneat|recurrent [--pop P] ...
+    python tools/bench_configs.py generation --gpus N --pop 1000000   (sharded, NCCL)
 """
 
 from __future__ import annotations
@@ -131,6 +132,44 @@ def bench_generation(a):
     return out
 
 
+def bench_generation_sharded(a):
+    """Config 3 over N GPUs: sharded_evolve_step (one rank per GPU, NCCL):
+    contiguous population shards, fitness / species-assignment all-gathers,
+    founding rounds, survivor-pool gather (distributed.py); gen/s is the
+    slowest rank's time per generation."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_01817_b200 as tn
+    from paper_2404_01817_b200 import distributed as dd
+    from paper_2404_01817_b200.runner import init_state
+    rank, world = dist.get_rank(), dist.get_world_size()
+    cfg = tn.NeatConfig(seed=0, pop_size=a.pop, inputs=2, outputs=1, problem="xor", max_nodes=50,
+                        max_conns=100, compatibility_threshold=1.0, max_species=10)
+    state = init_state(cfg)
+    lo, hi = dd.shard_range(a.pop, world, rank)
+    nodes, conns = state.population.nodes[lo:hi].contiguous(), state.population.conns[lo:hi].contiguous()
+    species = state.species
+    comm = dd.Collective()
+    ops = dd.DeviceOps(cfg)
+    problem = tn.make_problem(cfg)
+    root = tn.RngStream(cfg.seed)
+    times = []
+    for gen in range(a.gens):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = time.perf_counter()
+        nodes, conns, lo, species, stats = dd.sharded_evolve_step(nodes, conns, lo, species, cfg, root.child(gen),
+                                                                  state.allocator, problem, comm, ops)
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t], device="cuda", dtype=torch.float64)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        times.append(float(dt.item()))
+    return {"config": f"3: sharded generation pop {a.pop} over {world} GPUs (XOR, threshold 1.0)",
+            "gpus": world, "s_per_gen": times, "gen_per_s": 1.0 / times[-1], "species": len(species),
+            "best_fitness": stats.best_fitness}
+
+
 def bench_hyperneat(a):
     """Config 4: CPPN pop P x 4096 queries + tcgen05 substrate (S = 4096)."""
     import torch
@@ -225,6 +264,17 @@ def bench_recurrent(a):
 
 
 def main():
+    if "--gpus" in sys.argv and "WORLD_SIZE" not in os.environ:
+        n = int(sys.argv[sys.argv.index("--gpus") + 1])
+        if n > 1:  # one rank per GPU under torch.distributed.run
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                   "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+            import subprocess
+            raise SystemExit(subprocess.call(cmd))
     ap = argparse.ArgumentParser()
     ap.add_argument("which", choices=["xor", "generation", "hyperneat", "recurrent"])
     ap.add_argument("--pop", type=int, default=None)
@@ -233,11 +283,26 @@ def main():
     ap.add_argument("--sweeps", type=int, nargs="+", default=[1, 5, 10])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--ref-pop", type=int, default=0)
     a = ap.parse_args()
     defaults = {"xor": (1000, 100), "generation": (1_000_000, 3), "hyperneat": (10_000, 1),
                 "recurrent": (10_000, 1)}
     a.pop = a.pop or defaults[a.which][0]
     a.gens = a.gens or defaults[a.which][1]
+    if a.which == "generation" and "WORLD_SIZE" in os.environ:
+        import torch
+        import torch.distributed as dist
+        local = int(os.environ.get("LOCAL_RANK", 0))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        try:
+            out = bench_generation_sharded(a)
+            if dist.get_rank() == 0:
+                print(json.dumps(out), flush=True)
+        finally:
+            dist.destroy_process_group()
+        return
     out = {"xor": bench_xor, "generation": bench_generation, "hyperneat": bench_hyperneat,
            "recurrent": bench_recurrent}[a.which](a)
     print(json.dumps(out), flush=True)
