@@ -372,6 +372,12 @@ def gather_fitness(fit_local, fit_all, world: int) -> None:
         fit_all.copy_(fit_local)
 
 
+def _local_device() -> int:
+    """This rank's GPU.  TNEAT_BENCH_SHARE_GPU=1 (tests of the multi-rank path on
+    a one-GPU box, with TNEAT_BENCH_BACKEND=gloo) puts every rank on cuda:0."""
+    return 0 if os.environ.get("TNEAT_BENCH_SHARE_GPU") else int(os.environ.get("LOCAL_RANK", 0))
+
+
 def _free_port() -> int:
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
@@ -385,7 +391,7 @@ def run_ours(args, rank: int, world: int) -> None:
     import paper_2404_01817_b200 as tn
     from paper_2404_01817_b200.synthetic import synthetic_population
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", _local_device())
     torch.cuda.set_device(dev)
     total = args.pop
     lo, shard = shard_of(total, world, rank)
@@ -606,8 +612,12 @@ def main():
     torch.set_num_threads(max(1, min(8, (os.cpu_count() or 8) // max(1, world))))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+        torch.cuda.set_device(_local_device())
+        backend = os.environ.get("TNEAT_BENCH_BACKEND", "nccl")  # gloo: tests on a one-GPU box only
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", _local_device()))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world)
     finally:
