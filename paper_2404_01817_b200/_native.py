@@ -12,7 +12,9 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtneat.so")
+# TNEAT_LIB: an alternative build of the library (tools/build_variant.py, e.g.
+# the checked build with device bounds checks) for a whole test run
+LIB_PATH = os.environ.get("TNEAT_LIB") or os.path.join(_HERE, "libtneat.so")
 
 P, I32, I64, U64, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
 

@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace tneat {
@@ -264,6 +265,31 @@ template <typename T> __device__ __forceinline__ T agg_finish(int agg, T acc, in
   if (count == 0) return T(0);
   if (agg == AGG_MEAN) return acc / T(count);
   return acc;
+}
+
+// Checked builds (-DTNEAT_CHECKS, tools/build_variant.py checks): device-side
+// bounds checks on every shared-memory carve, staged program index and
+// program write; a violation prints its site and traps (the launch fails with
+// an error the host raises).  compute-sanitizer is closed on this GPU pool.
+#ifdef TNEAT_CHECKS
+#define TNEAT_DCHECK(cond, what, a, b)                                                                      \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("TNEAT_CHECK failed: %s (%lld, %lld) at %s:%d block %d thread %d\n", what, (long long)(a),   \
+             (long long)(b), __FILE__, __LINE__, (int)blockIdx.x, (int)threadIdx.x);                       \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define TNEAT_DCHECK(cond, what, a, b) \
+  do {                                 \
+  } while (0)
+#endif
+
+__device__ __forceinline__ uint32_t dynamic_smem_bytes() {
+  uint32_t r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
 }
 
 }  // namespace tneat

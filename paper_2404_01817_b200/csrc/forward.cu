@@ -494,6 +494,22 @@ __device__ __forceinline__ void tile_task(const uint8_t* __restrict__ prog, cons
   float* w_s = reinterpret_cast<float*>(smem + off_w);
   EdgeD* ed_s = reinterpret_cast<EdgeD*>(smem + off_w);
   T* vals = reinterpret_cast<T*>(smem + align_up(off_w + w_bytes, 16));
+  TNEAT_DCHECK(align_up(off_w + w_bytes, 16) + (int64_t)hdr.n_slots * RB <= (int64_t)dynamic_smem_bytes(),
+               "tile program + value slots fit shared memory", hdr.n_slots, dynamic_smem_bytes());
+#ifdef TNEAT_CHECKS
+  if (sizeof(T) == 4) {  // every entry a sum group sweeps reads a value slot
+    const uint16_t* gsrc = reinterpret_cast<const uint16_t*>(gp + L.off_src);
+    const GroupRec* grs = reinterpret_cast<const GroupRec*>(gp + L.off_groups);
+    for (int g = threadIdx.x; g < n_groups; g += blockDim.x) {
+      const GroupRec r = grs[g];
+      const int gw = group_width(r.n);
+      if (r.cls & GRP_GENERIC) continue;
+      TNEAT_DCHECK(r.e_begin + gw * r.rounds <= n_edges, "tile group record", r.e_begin + gw * r.rounds, n_edges);
+      for (int e = r.e_begin; e < r.e_begin + gw * r.rounds; ++e)
+        TNEAT_DCHECK(gsrc[e] < hdr.n_slots, "tile edge source slot", gsrc[e], hdr.n_slots);
+    }
+  }
+#endif
   if (sizeof(T) == 4 && tid == 0 && (((uintptr_t)in | (uint32_t)(I * 4) | (uint64_t)in_gstride * 4) & 15) == 0) {
     const int t0 = run * tpc * TT;  // first tile of this CTA: in flight while the program is staged
     if (t0 < B) prefetch_l2(in + gi * in_gstride + (int64_t)t0 * I, (uint32_t)(min(TT, B - t0) * I * 4));
@@ -1007,6 +1023,22 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
     const float* gin = in + gi * in_gstride;
     float* go = out + gi * out_gstride;
     const int zc = in_gstride ? (int)gi : 0;  // input tensor map: (I, B, genomes)
+    TNEAT_DCHECK(n_steps == 0 || (tb.bytes + 64 <= gbuf_bytes), "tc genome block fits its buffer", tb.bytes, gbuf_bytes);
+    TNEAT_DCHECK(nb <= nb_max, "tc MMA width within the class", nb, nb_max);
+    TNEAT_DCHECK((uint32_t)(n_steps + 1) * TC_RB <= wg_bytes, "tc value slots fit the warpgroup area", n_steps, wg_bytes);
+#ifdef TNEAT_CHECKS
+    for (int g = tid; g < n_groups; g += blockDim.x) {  // every entry a group sweeps reads a value slot
+      const uint4 r = reinterpret_cast<const uint4*>(gr_s)[g];
+      const uint32_t n = (r.x & 3) + 1, gw = n == 3 ? 4 : n;
+      TNEAT_DCHECK(r.z + gw * r.y <= (uint32_t)n_edges && r.w + n <= (uint32_t)n_steps, "tc group record",
+                   r.z + gw * r.y, n_edges);
+      for (uint32_t e = r.z; e < r.z + gw * r.y; ++e)
+        TNEAT_DCHECK(src_s[e] <= (uint32_t)n_steps * TC_RB && (src_s[e] % TC_RB) == 0, "tc hidden source slot",
+                     src_s[e], n_steps);
+    }
+    TNEAT_DCHECK(smem_u32(gb) + tb.bytes + 64 <= smem_u32(smem) + dynamic_smem_bytes(), "tc block in smem",
+                 tb.bytes, dynamic_smem_bytes());
+#endif
     const bool pf_l2 = ((uintptr_t)gin & 15) == 0;
     const uint16_t* in_start = reinterpret_cast<const uint16_t*>(gp + L.off_in);
     const uint16_t* isrc = reinterpret_cast<const uint16_t*>(gp + L.off_isrc);
@@ -1056,6 +1088,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
             __nanosleep(32);
           }
         }
+        TNEAT_DCHECK(slot < n_slots && (slot + 1) * slot_cols <= 512u, "tc TMEM slot", slot, n_slots);
         sh.slot_col[wg] = slot * slot_cols;
       }
       tc_fence_before();

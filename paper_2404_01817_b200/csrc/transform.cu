@@ -963,6 +963,10 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     const int r = lookup_row(s.skey, Npad, (uint64_t)(I + o));
     out_slot[o] = r >= 0 ? s.slot_of[r] : NO_SLOT;
   }
+  TNEAT_DCHECK(e_total <= edge_capacity(N, C), "program edge entries within capacity", e_total, edge_capacity(N, C));
+  TNEAT_DCHECK(!tc_ok || L.off_tc + tb.bytes <= L.off_in, "tc block within its area", tb.bytes, L.off_in - L.off_tc);
+  TNEAT_DCHECK(!tc_ok || n_emit <= 128, "tc steps", n_emit, 128);
+  TNEAT_DCHECK(tc_ok || n_slots <= N + 2, "standard value slots", n_slots, N + 2);
   if (lane == 0) {
     ProgHeader h{n_emit, e_total, n_slots, n_order, status, n_live, tc_ok ? (int)MODE_TC : mode, n_groups};
     *hdr = h;

@@ -131,3 +131,21 @@ def upload_async(arr: np.ndarray, dev: torch.device) -> tuple[torch.Tensor, torc
 
 def ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else int(t.data_ptr())
+
+
+class nvtx:
+    """NVTX range around a host phase (visible in nsys / ncu timelines; a
+    no-op cost of ~100 ns without a profiler attached)."""
+
+    __slots__ = ("name",)
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        torch.cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        torch.cuda.nvtx.range_pop()
+        return False

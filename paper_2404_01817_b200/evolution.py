@@ -616,11 +616,13 @@ def evolve_step(pop: PopulationTensors, species: list, config: NeatConfig, rng, 
                 problem, registry=None, threads: int = 1, sequential: bool = False):
     """Evaluate, then stagnate, allocate, reproduce and re-speciate
     (evolution.py:722-773).  ``rng`` is scoped to the generation."""
+    from .device import nvtx
     registry = registry or DEFAULT_REGISTRY
     start = time.perf_counter()
-    fitness = np.asarray(problem.evaluate_population_tensors(pop, registry, rng.child(STAGE_EVAL),
-                                                             threads=threads, sequential=sequential),
-                         dtype=np.float64)
+    with nvtx("evolve_step.evaluate"):
+        fitness = np.asarray(problem.evaluate_population_tensors(pop, registry, rng.child(STAGE_EVAL),
+                                                                 threads=threads, sequential=sequential),
+                             dtype=np.float64)
     evaluated = PopulationTensors(pop.nodes, pop.conns, pop.species_id, fitness, pop.num_inputs,
                                   pop.num_outputs)
     nd, cd = _dev64(pop.nodes), _dev64(pop.conns)
@@ -643,13 +645,16 @@ def evolve_step(pop: PopulationTensors, species: list, config: NeatConfig, rng, 
         stats.solved = True
         stats.elapsed_seconds = time.perf_counter() - start
         return evaluated, species, stats
-    survivors = update_stagnation(species, fitness, config)
-    if not survivors:
-        raise ExtinctionError("all species stagnated; increase species_elitism")
-    allocated = allocate_spawns(survivors, fitness, config)
-    offspring = reproduce(evaluated, allocated, fitness, config, rng, allocator, threads=threads,
-                          sequential=sequential)
-    new_pop, new_species = speciate(offspring, allocated, config, rng.child(STAGE_SPECIATE),
-                                    sequential=sequential)
+    with nvtx("evolve_step.stagnation_spawns"):
+        survivors = update_stagnation(species, fitness, config)
+        if not survivors:
+            raise ExtinctionError("all species stagnated; increase species_elitism")
+        allocated = allocate_spawns(survivors, fitness, config)
+    with nvtx("evolve_step.reproduce"):
+        offspring = reproduce(evaluated, allocated, fitness, config, rng, allocator, threads=threads,
+                              sequential=sequential)
+    with nvtx("evolve_step.speciate"):
+        new_pop, new_species = speciate(offspring, allocated, config, rng.child(STAGE_SPECIATE),
+                                        sequential=sequential)
     stats.elapsed_seconds = time.perf_counter() - start
     return new_pop, new_species, stats

@@ -40,7 +40,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .device import upload_async, device, ptr, stream_handle, to_device
+from .device import nvtx, upload_async, device, ptr, stream_handle, to_device
 from .errors import ConfigError, CycleDetected, IntegrityError, InvalidInput
 from .functions import DEFAULT_REGISTRY, check_registry
 
@@ -245,6 +245,12 @@ def transform_arrays(nodes, conns, num_inputs: int, num_outputs: int, *,
         raise ConfigError("layout='tc' needs fp32 feed-forward programs with <= 32 inputs (a multiple of 4)")
     if layout in ("tc", "auto") and tc_ok:
         prec |= FMT_TC
+    with nvtx("transform_arrays"):
+        return _transform_arrays(nd, cd, num_inputs, num_outputs, prec, mode, prune, stream, sync, with_order)
+
+
+def _transform_arrays(nd, cd, num_inputs, num_outputs, prec, mode, prune, stream, sync, with_order):
+    pop, n, c = int(nd.shape[0]), int(nd.shape[1]), int(cd.shape[1])
     stride = int(_native.lib().an_program_stride(n, c, num_outputs, prec))
     dev = nd.device
     program = torch.empty((pop, stride), dtype=torch.uint8, device=dev)

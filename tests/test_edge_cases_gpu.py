@@ -89,3 +89,46 @@ def test_large_genome_capacity(tn):
     out = tn.forward_arrays(st32, None, x.astype(np.float32))
     ref = _oracle_out(nodes, conns, x, 16, 4)
     assert np.max(np.abs(out - ref) / np.maximum(1.0, np.abs(ref))) <= 1e-5
+
+
+def test_checked_build_traps_on_a_corrupt_program(tmp_path):
+    """The checked build (-DTNEAT_CHECKS, run with TNEAT_LIB=...libtneat_checks.so)
+    validates staged program indices on the device: a program whose hidden
+    edge points past the genome's value slots makes the launch fail instead
+    of reading out of bounds.  (Run in a subprocess: a trap poisons the context.)"""
+    import os
+    import subprocess
+    import sys
+    lib = os.environ.get("TNEAT_LIB", "")
+    if "checks" not in lib:
+        pytest.skip("checked build not selected (TNEAT_LIB)")
+    code = r"""
+import sys, torch
+sys.path.insert(0, %r)
+import paper_2404_01817_b200 as tn
+from paper_2404_01817_b200.synthetic import synthetic_population
+n, c = synthetic_population(4, 128, 512, 32, 8, seed=5)
+st, _ = tn.transform_arrays(n, c, 32, 8)
+L = tn.inference
+hdr = st.program[:, :32].contiguous().view(torch.int32)
+steps, edges, groups = (int(v) for v in hdr[0, [0, 1, 7]])
+off = 128  # off_tc for O = 8
+nb = (steps + 15) // 16 * 16
+grp = off + 192 * nb + 4 * nb
+recs = st.program[0, grp:grp + 16 * groups].contiguous().view(torch.int32).view(-1, 4).cpu()
+e = int(next(r[2] for r in recs if r[1] > 0))  # first entry a group actually sweeps
+src = grp + 16 * groups + 16 * steps + 4 * e
+st.program[0, src:src + 4] = torch.tensor([0, 0, 0x7F, 0], dtype=torch.uint8)  # slot far past n_steps
+x = torch.randn(4, 256, 32, device="cuda")
+try:
+    tn.forward_device(st, x)
+    torch.cuda.synchronize()
+    print("NO-TRAP")
+except Exception as e:
+    print("TRAPPED", type(e).__name__)
+""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),)
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                         env=dict(os.environ))
+    out = res.stdout + res.stderr
+    assert "NO-TRAP" not in out, out[-2000:]
+    assert "TNEAT_CHECK failed" in out, out[-2000:]
