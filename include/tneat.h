@@ -82,7 +82,7 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
  *            (FMT_TC programs whose header mode is 2; persistent, one CTA per
  *            SM; bits 8..11 = maximum warpgroups per CTA, 0 = as many as
  *            fit).  In an FMT_TC population the other variants take the
- *            standard-program genomes only.  Bits 8..15 = tiles per CTA for
+ *            standard-program genomes only, listed in genome_ids (-7 without).  Bits 8..15 = tiles per CTA for
  *            the tile kernels (0 = 4) */
 int an_forward(const void* program, int64_t program_stride, int N, int C, int precision,
                const int32_t* maxdims_host, const int32_t* genome_ids, const void* inputs,

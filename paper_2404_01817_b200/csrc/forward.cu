@@ -1114,7 +1114,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
 #ifdef TNEAT_DIAG_TC_NOEPI  // diagnostic builds only: no TMEM -> slot epilogue
         for (int c = 0; c < 0; c += 8) {
 #else
-        for (int c = 0; c < nb; c += 8) {
+        for (int c = 0; c < n_steps; c += 8) {  // columns past the last step are not read
 #endif
           uint32_t a4[8], a3[8], b4[8], b3[8];
           TMEM_LD8(t_lane + (uint32_t)c, a4);
@@ -1728,6 +1728,9 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
                      (float*)outputs, ogs, tpc & 0xF, st);
   }
   if (tpc == 0) tpc = 4;
+  // an FMT_TC population holds tensor-core programs the standard kernels cannot
+  // read: they take explicitly listed standard-program genomes only
+  if ((precision & FMT_TC) && !genome_ids) return -7;
   if (variant == 0) variant = B >= 192 ? 5 : (B >= 96 ? 3 : 8);
   if (variant == 8) {
     if (genome_ids) return -7;

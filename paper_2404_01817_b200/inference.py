@@ -69,7 +69,7 @@ class StackedNetworks:
     num_outputs: int
     program: torch.Tensor            # (P, stride) uint8
     order_dev: torch.Tensor | None   # (P, N) int16, -1 padded; computed on first use
-    conn_rows: torch.Tensor          # (P, C, 2) int16
+    conn_rows_dev: torch.Tensor | None  # (P, C, 2) int16; computed on first use
     io_rows: torch.Tensor            # (P, I+O) int32
     status_dev: torch.Tensor         # (P,) int32
     maxdims: tuple[int, int, int]    # max (slots, steps, edges) over the population
@@ -105,6 +105,24 @@ class StackedNetworks:
         if "nodes" not in self._cache:
             self._cache["nodes"] = self.nodes_dev.cpu().numpy()
         return self._cache["nodes"]
+
+    @property
+    def conn_rows(self) -> torch.Tensor:
+        """(P, C, 2) int16 (src row, dst row) of the enabled connections that
+        enter the reference's dense incoming (-1 elsewhere).  Programs do not
+        need it, so it is computed on first use by a transform pass that also
+        emits it."""
+        if self.conn_rows_dev is None:
+            p, n, c = self.size, self.max_nodes, self.max_conns
+            rows = torch.empty((p, c, 2), dtype=torch.int16, device=self.program.device)
+            scratch = torch.empty_like(self.program)
+            status = torch.zeros((p,), dtype=torch.int32, device=self.program.device)
+            md = torch.zeros((3,), dtype=torch.int32, device=self.program.device)
+            _native.call("an_transform", ptr(self.nodes_dev), ptr(self.conns_dev), p, n, c, self.num_inputs,
+                         self.num_outputs, self.mode, self.precision, 1, ptr(scratch), self.stride, None,
+                         ptr(rows), None, ptr(status), ptr(md), stream_handle())
+            self.conn_rows_dev = rows
+        return self.conn_rows_dev
 
     def order_device(self) -> torch.Tensor:
         """The reference's Kahn order (P, N) int16 on the device.  Programs do not
@@ -164,7 +182,8 @@ class StackedNetworks:
         sub = StackedNetworks(self.nodes_dev[idx], self.conns_dev[idx], self.num_inputs,
                               self.num_outputs, self.program[idx],
                               None if self.order_dev is None else self.order_dev[idx],
-                              self.conn_rows[idx], self.io_rows[idx], self.status_dev[idx],
+                              None if self.conn_rows_dev is None else self.conn_rows_dev[idx],
+                              self.io_rows[idx], self.status_dev[idx],
                               self.maxdims, self.precision, self.mode)
         if isinstance(idx, slice):
             for k in ("status", "slots", "steps_edges", "modes"):
@@ -182,7 +201,8 @@ class StackedNetworks:
         cat = lambda name: torch.cat([getattr(p, name) for p in parts])  # noqa: E731
         order = None if any(p.order_dev is None for p in parts) else cat("order_dev")
         return cls(cat("nodes_dev"), cat("conns_dev"), first.num_inputs, first.num_outputs,
-                   cat("program"), order, cat("conn_rows"), cat("io_rows"),
+                   cat("program"), order,
+                   None if any(p.conn_rows_dev is None for p in parts) else cat("conn_rows_dev"), cat("io_rows"),
                    cat("status_dev"), md, first.precision, first.mode)
 
 
@@ -255,15 +275,14 @@ def _transform_arrays(nd, cd, num_inputs, num_outputs, prec, mode, prune, stream
     dev = nd.device
     program = torch.empty((pop, stride), dtype=torch.uint8, device=dev)
     order = torch.empty((pop, n), dtype=torch.int16, device=dev) if with_order else None
-    conn_rows = torch.empty((pop, c, 2), dtype=torch.int16, device=dev)
     io_rows = torch.empty((pop, num_inputs + num_outputs), dtype=torch.int32, device=dev)
     status = torch.zeros((pop,), dtype=torch.int32, device=dev)
     maxdims = torch.zeros((3,), dtype=torch.int32, device=dev)
     _native.call("an_transform", ptr(nd), ptr(cd), pop, n, c, num_inputs, num_outputs, mode, prec,
                  int(bool(prune)), ptr(program), stride, ptr(order) if order is not None else None,
-                 ptr(conn_rows), ptr(io_rows),
+                 None, ptr(io_rows),
                  ptr(status), ptr(maxdims), stream_handle(stream))
-    stacked = StackedNetworks(nd, cd, num_inputs, num_outputs, program, order, conn_rows, io_rows,
+    stacked = StackedNetworks(nd, cd, num_inputs, num_outputs, program, order, None, io_rows,
                               status, (0, 0, 0), prec, mode)
     stacked._cache["maxdims_dev"] = maxdims
     if not sync:
