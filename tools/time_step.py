@@ -54,3 +54,13 @@ for _ in range(a.fwd_reps):
     evs.append(e0.elapsed_time(e1))
 evs.sort()
 print(f"{a.lib or 'libtneat.so'} forward median {evs[len(evs) // 2]:.3f} ms min {evs[0]:.3f} ms", flush=True)
+tvs = []
+for _ in range(a.fwd_reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    tn.transform_arrays(nodes, conns, 32, 8, sync=False, layout=a.layout)
+    e1.record()
+    torch.cuda.synchronize()
+    tvs.append(e0.elapsed_time(e1))
+tvs.sort()
+print(f"{a.lib or 'libtneat.so'} transform median {tvs[len(tvs) // 2]:.3f} ms min {tvs[0]:.3f} ms", flush=True)
