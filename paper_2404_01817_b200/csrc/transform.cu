@@ -291,6 +291,9 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   const bool recurrent = mode == 1;
   int status = 0;
 
+#if defined(XSTOP) && XSTOP == 6
+  if (lane < 32) return;
+#endif
   // ---- nodes: live mask, key table ------------------------------------------
   int n_live = 0;
   for (int r = lane; r < Npad; r += 32) {
@@ -330,6 +333,9 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   __syncwarp();
   warp_bitonic_sort(s.skey, Npad);
 
+#if defined(XSTOP) && XSTOP == 7
+  if (lane < 32) return;
+#endif
   // ---- conns: endpoint rows, enabled mask, compacted edge keys ----------------
   int n_en = 0;
   for (int base = 0; base < C; base += 32) {
@@ -363,6 +369,9 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   }
   __syncwarp();
 
+#if defined(XSTOP) && XSTOP == 1
+  if (lane < 32) return;
+#endif
   // ---- counting sort by destination, then by source inside each bucket; CSR by
   // destination (in_start) and by source (su_start/succ) ------------------------
   for (int e = lane; e < n_en; e += 32) {
@@ -442,6 +451,9 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   for (int r = lane; r < N; r += 32) s.lvl[r] = 0;
   __syncwarp();
 
+#if defined(XSTOP) && XSTOP == 2
+  if (lane < 32) return;
+#endif
   // ---- Kahn, smallest ready row first (inference.py:127-141) + levels ---------
   const int W = (N + 31) / 32;
   for (int w = 0; w < W; ++w) {
@@ -519,6 +531,9 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   }
   if (n_order < n_live) status |= ST_CYCLIC;
 
+#if defined(XSTOP) && XSTOP == 3
+  if (lane < 32) return;
+#endif
   // ---- order / io rows outputs -----------------------------------------------
   if (order_out) {
     for (int i = lane; i < N; i += 32)
@@ -599,15 +614,33 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       if (emit) {
         const double gv = gn[(int64_t)r * 5 + 3];
         if (!(gv == (double)AGG_SUM || gv == (double)AGG_MEAN)) bad = 1;
-        double mw = 0.0;
+        // one pass, weights loaded 4 at a time: the input-weight maximum, and
+        // the hidden-weight maximum / smallest nonzero magnitude
+        double mw = 0.0, hmax = 0.0, hmin = INFINITY;
         int cin = 0;
-        for (int e = s.in_start[r]; e < s.in_start[r + 1]; ++e) {
-          const typename KT::E kk = s.ekey[e];
-          if (s.flags[KT::src(kk)] & F_INPUT) {
-            const double w = gc[KT::row(kk) * 4 + 3];
-            if (!isfinite(w)) bad = 1;
-            mw = fmax(mw, fabs(w));
-            ++cin;
+        const int e1 = s.in_start[r + 1];
+        for (int e = s.in_start[r]; e < e1; e += 4) {
+          double w[4];
+          bool inp[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const typename KT::E kk = s.ekey[e + u < e1 ? e + u : e];
+            inp[u] = (s.flags[KT::src(kk)] & F_INPUT) != 0;
+            w[u] = __ldg(gc + KT::row(kk) * 4 + 3);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (e + u >= e1) break;
+            const double a = fabs(w[u]);
+            if (inp[u]) {
+              if (!isfinite(w[u])) bad = 1;
+              mw = fmax(mw, a);
+              ++cin;
+            } else {
+              hmax = fmax(hmax, a);  // NaN: fails the range test below through hmin
+              if (a != 0.0) hmin = fmin(hmin, a);
+              if (isnan(a)) bad = 1;
+            }
           }
         }
         if (mw != 0.0 && (mw < 0x1p-62 || mw >= 0x1p63)) bad = 1;
@@ -617,11 +650,19 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
         const int ewx = mw != 0.0 ? ilogb(mw) : 12;
         s.su_start[r] = ewx;
         const double up = ldexp(1.0, 12 - ewx), dn = ldexp(1.0, ewx - 12);
-        for (int e = s.in_start[r]; e < s.in_start[r + 1]; ++e) {
-          const typename KT::E kk = s.ekey[e];
-          if (!(s.flags[KT::src(kk)] & F_INPUT)) {
-            const double w = fabs(gc[KT::row(kk) * 4 + 3]) * up;
-            if (!(w < 0x1p100) || (w != 0.0 && w < 0x1p-100)) bad = 1;
+        if (!(hmax * up < 0x1p100)) bad = 1;
+        if (hmin != INFINITY) {
+          const double lo = hmin * up;
+          if (lo != 0.0) {
+            if (lo < 0x1p-100) bad = 1;
+          } else {  // the smallest weight underflows (reads as 0): test each (rare)
+            for (int e = s.in_start[r]; e < e1; ++e) {
+              const typename KT::E kk = s.ekey[e];
+              if (!(s.flags[KT::src(kk)] & F_INPUT)) {
+                const double w = fabs(gc[KT::row(kk) * 4 + 3]) * up;
+                if (w != 0.0 && w < 0x1p-100) bad = 1;
+              }
+            }
           }
         }
         const double rs = fabs(gn[(int64_t)r * 5 + 2]) * dn;
@@ -633,6 +674,9 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   }
   __syncwarp();
 
+#if defined(XSTOP) && XSTOP == 4
+  if (lane < 32) return;
+#endif
   // ---- steps: emitted nodes sorted by (level, class, -count, position) --------
   // feed-forward: positions in the Kahn order; recurrent: rows (all nodes are
   // state, singleton groups, no slot recycling).  TC programs group by the
@@ -817,6 +861,9 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     for (int k = lane; k <= n_emit; k += 32) in_start[k] = (uint16_t)s.last_grp[k];
   }
 
+#if defined(XSTOP) && XSTOP == 5
+  if (lane < 32) return;
+#endif
   // ---- write groups, steps and interleaved edge lists --------------------------
   // (TC programs: into the staged block, common.cuh tc_block)
   const TcBlock tb = tc_block(n_emit, n_groups, e_total);
@@ -890,27 +937,38 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
 #pragma unroll 1
         for (int q = 0; q < 12; ++q) *(uint4*)(brow + tc_offset(k, 8 * q)) = make_uint4(0, 0, 0, 0);
         int hc = 0, ic = s.last_grp[k];
-        const int c0 = gr.cnt[0];
-        for (int e = e0; e < e0 + cnt; ++e) {
-          const typename KT::E kk = s.ekey[e];
-          const int sr = KT::src(kk);
-          const double w = gc[KT::row(kk) * 4 + 3];
-          if (s.flags[sr] & F_INPUT) {
-            const int idx = (int)gn[(int64_t)sr * 5];
-            isrc[ic] = (uint16_t)idx;
-            iw[ic] = (float)w;
-            ++ic;
-            double d2, d1, d0;
-            digits3_d(w * sc, d2, d1, d0);
-            *(__half*)(brow + tc_offset(k, idx)) = __double2half(d2);
-            *(__half*)(brow + tc_offset(k, TC_K + idx)) = __double2half(d1);
-            *(__half*)(brow + tc_offset(k, 2 * TC_K + idx)) = __double2half(d0);
-          } else {
-            int col = j, rr = hc;
-            if (split0 && j == 0 && hc >= c0) { col = 3; rr = hc - c0; }
-            esrc[gr.e_begin + rr * gw + col] = (uint32_t)s.slot_of[sr] * TC_SLOT_BYTES;
-            ew[gr.e_begin + rr * gw + col] = (float)(w * up);
-            ++hc;
+        const int c0 = gr.cnt[0], e1 = e0 + cnt;
+        // edges 4 at a time: their weight (and input index) loads are in flight
+        // together; identity io rows (io_fast) need no index load at all
+        for (int e = e0; e < e1; e += 4) {
+          double w[4];
+          int sr[4], idx[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const typename KT::E kk = s.ekey[e + u < e1 ? e + u : e];
+            sr[u] = KT::src(kk);
+            w[u] = __ldg(gc + KT::row(kk) * 4 + 3);
+            idx[u] = io_fast ? sr[u] : (int)__ldg(gn + (int64_t)sr[u] * 5);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (e + u >= e1) break;
+            if (s.flags[sr[u]] & F_INPUT) {
+              isrc[ic] = (uint16_t)idx[u];
+              iw[ic] = (float)w[u];
+              ++ic;
+              double d2, d1, d0;
+              digits3_d(w[u] * sc, d2, d1, d0);
+              *(__half*)(brow + tc_offset(k, idx[u])) = __double2half(d2);
+              *(__half*)(brow + tc_offset(k, TC_K + idx[u])) = __double2half(d1);
+              *(__half*)(brow + tc_offset(k, 2 * TC_K + idx[u])) = __double2half(d0);
+            } else {
+              int col = j, rr = hc;
+              if (split0 && j == 0 && hc >= c0) { col = 3; rr = hc - c0; }
+              esrc[gr.e_begin + rr * gw + col] = (uint32_t)s.slot_of[sr[u]] * TC_SLOT_BYTES;
+              ew[gr.e_begin + rr * gw + col] = (float)(w[u] * up);
+              ++hc;
+            }
           }
         }
         continue;
