@@ -13,31 +13,43 @@
 //   * environment: s_{t+1} = tanh(A s_t + M a_t),
 //     A (D x D), M (D x O) shared; observation = s_t, action a_t = outputs
 //     after the K sweeps, reward = s_t[0]; fitness = sum over T steps.
-// Lanes own nodes (a sweep is max-in-degree deep, not node-count deep) and
-// environment rows; the warp needs no block barrier.
+// Lanes own nodes (a sweep is max-in-degree deep, not node-count deep; nodes
+// sorted by in-degree so the 32 deepest share one iteration) and environment
+// rows; the warp needs no block barrier.
 
 #include "common.cuh"
 
 namespace tneat {
 
-template <typename T>
-__device__ __forceinline__ T node_value(const StepT<T>& st, T acc, int count);
-template <>
-__device__ __forceinline__ float node_value<float>(const StepT<float>& st, float acc, int count) {
-  const float a = agg_finish<float>(st.agg, acc, count);
-  return apply_act(st.act, fmaf(st.resp, a, st.bias));
-}
-template <>
-__device__ __forceinline__ double node_value<double>(const StepT<double>& st, double acc, int count) {
-  return apply_act(st.act, fma(st.resp, agg_finish<double>(st.agg, acc, count), st.bias));
-}
-
 // shared memory of one warp: value buffers, environment vectors, then the
-// genome's step records and its edges compacted to the steps' real counts
+// genome's nodes in descending in-degree order and their edges as packed
+// (source byte offset, weight) pairs
+template <typename T>
+struct __align__(8) RecEdge {
+  uint32_t off;  // source slot * sizeof(T)
+  T w;
+};
+template <typename T>
+struct __align__(16) RecNode {
+  uint16_t slot, count, e_begin;
+  uint8_t act, agg;
+  T bias, resp;
+};
 template <typename T>
 __host__ __device__ inline int64_t rollout_warp_bytes(int slots, int D, int O, int max_n, int max_e) {
-  return align_up((2ll * slots + 2ll * D + O) * (int64_t)sizeof(T), 16) + (int64_t)max_n * sizeof(StepT<T>) +
-         align_up((int64_t)max_e * sizeof(T), 16) + align_up(2ll * max_e, 16);
+  return align_up((2ll * slots + 2ll * D + O) * (int64_t)sizeof(T), 16) + (int64_t)max_n * sizeof(RecNode<T>) +
+         align_up((int64_t)max_e * sizeof(RecEdge<T>), 16);
+}
+
+template <typename T>
+__device__ __forceinline__ T node_sum_act(const RecNode<T>& nd, T acc);
+template <>
+__device__ __forceinline__ float node_sum_act<float>(const RecNode<float>& nd, float acc) {
+  return tanh_fast(fmaf(nd.resp, acc, nd.bias));
+}
+template <>
+__device__ __forceinline__ double node_sum_act<double>(const RecNode<double>& nd, double acc) {
+  return tanh(fma(nd.resp, acc, nd.bias));
 }
 
 template <typename T>
@@ -61,9 +73,8 @@ __global__ void rollout_kernel(const uint8_t* __restrict__ prog, ProgLayout L, i
   T* s = buf1 + slots;        // environment state (D)
   T* s_next = s + D;          // (D)
   T* act = s_next + D;        // actions (O)
-  StepT<T>* rec = reinterpret_cast<StepT<T>*>(wbase + align_up((2ll * slots + 2ll * D + O) * (int64_t)sizeof(T), 16));
-  T* wt = reinterpret_cast<T*>(rec + max_n);
-  uint16_t* srcs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(wt) + align_up((int64_t)max_e * sizeof(T), 16));
+  RecNode<T>* nodes = reinterpret_cast<RecNode<T>*>(wbase + align_up((2ll * slots + 2ll * D + O) * (int64_t)sizeof(T), 16));
+  RecEdge<T>* edges = reinterpret_cast<RecEdge<T>*>(nodes + max_n);
   const uint8_t* gp = prog + gi * L.stride;
   const ProgHeader hdr = *reinterpret_cast<const ProgHeader*>(gp);
   const StepT<T>* stp = reinterpret_cast<const StepT<T>*>(gp + L.off_steps);
@@ -73,33 +84,59 @@ __global__ void rollout_kernel(const uint8_t* __restrict__ prog, ProgLayout L, i
   const EdgeD* ed = reinterpret_cast<const EdgeD*>(gp + L.off_w);
   const uint16_t* out_slot = reinterpret_cast<const uint16_t*>(gp + L.off_out);
   const int n_steps = hdr.n_steps;
-  // stage the program: step records (pad = compact first edge) and the edges
-  // of every step back to back (recurrent programs: singleton groups, step j =
-  // group j)
+  // stage the program (recurrent programs: singleton groups, step j = group j):
+  // position of step j = its rank by (in-degree descending, j) -- lanes take
+  // positions lane, lane + 32, ...: the warp's edge rounds per sweep are the
+  // sum over those iterations of the largest degree, which this order
+  // minimises.  A node's edges keep their program order (the sum's order).
+  for (int j = lane; j < n_steps; j += 32) {
+    const int cj = stp[j].count;
+    int rank = 0;
+    for (int k = 0; k < n_steps; ++k) {
+      const int ck = stp[k].count;
+      rank += (ck > cj || (ck == cj && k < j)) ? 1 : 0;
+    }
+    buf0[j] = (T)rank;  // scratch: the value buffers are cleared below
+  }
+  __syncwarp();
+  // edge offsets: exclusive scan of the counts in position order, each list
+  // starting at an even record (two records = one 16-byte load for fp32)
   int carry = 0;
   for (int base = 0; base < n_steps; base += 32) {
-    const int j = base + lane;
-    StepT<T> st;
-    int c = 0;
-    if (j < n_steps) { st = stp[j]; c = st.count; }
+    const int p = base + lane;
+    int j = -1;
+    for (int k = 0; k < n_steps && p < n_steps; ++k)
+      if ((int)buf0[k] == p) { j = k; break; }
+    const int c = j >= 0 ? ((int)stp[j].count + 1) & ~1 : 0;
     int x = c;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, x, d);
       if (lane >= d) x += y;
     }
-    if (j < n_steps) {
+    if (j >= 0) {
+      const StepT<T> st = stp[j];
       const int c0 = carry + x - c;
-      st.pad = (uint16_t)c0;
-      rec[j] = st;
+      RecNode<T> nd;
+      nd.slot = st.slot;
+      nd.count = st.count;
+      nd.e_begin = (uint16_t)c0;
+      nd.act = st.act;
+      nd.agg = st.agg;
+      nd.bias = st.bias;
+      nd.resp = st.resp;
+      nodes[p] = nd;
       const int g0 = grp[j].e_begin;
-      for (int e = 0; e < c; ++e) {
-        if constexpr (sizeof(T) == 8) { srcs[c0 + e] = (uint16_t)ed[g0 + e].src; wt[c0 + e] = (T)ed[g0 + e].w; }
-        else { srcs[c0 + e] = esrc[g0 + e]; wt[c0 + e] = (T)ew[g0 + e]; }
+      for (int e = 0; e < (int)st.count; ++e) {
+        RecEdge<T> r;
+        if constexpr (sizeof(T) == 8) { r.off = ed[g0 + e].src * (uint32_t)sizeof(T); r.w = (T)ed[g0 + e].w; }
+        else { r.off = (uint32_t)esrc[g0 + e] * (uint32_t)sizeof(T); r.w = (T)ew[g0 + e]; }
+        edges[c0 + e] = r;
       }
     }
     carry += __shfl_sync(0xffffffffu, x, 31);
   }
+  __syncwarp();
   for (int i = lane; i < slots; i += 32) { buf0[i] = T(0); buf1[i] = T(0); }
   for (int i = lane; i < D; i += 32) s[i] = s0[i];
   __syncwarp();
@@ -115,18 +152,53 @@ __global__ void rollout_kernel(const uint8_t* __restrict__ prog, ProgLayout L, i
     }
     __syncwarp();
     for (int k = 0; k < sweeps; ++k) {
-      for (int j = lane; j < n_steps; j += 32) {
-        const StepT<T> st = rec[j];
-        const int e0 = st.pad;
-        T acc;
-        if (st.agg == AGG_SUM || st.agg == AGG_MEAN) {  // (mean divides in node_value)
-          acc = T(0);
-          for (int e = 0; e < st.count; ++e) acc = acc + wt[e0 + e] * cur[srcs[e0 + e]];
+      const char* cb = reinterpret_cast<const char*>(cur);
+      for (int p = lane; p < n_steps; p += 32) {
+        const RecNode<T> nd = nodes[p];
+        const RecEdge<T>* er = edges + nd.e_begin;
+        const int cnt = nd.count;
+        T v;
+        if (nd.agg == AGG_SUM && nd.act == ACT_TANH) {  // the common node: inline, edges two at a time
+          T acc = T(0);
+          int e = 0;
+          // four edges per iteration: the record and value loads of the four are
+          // in flight together; the sum keeps the edge order
+          for (; e + 4 <= cnt; e += 4) {
+            RecEdge<T> r[4];
+            if constexpr (sizeof(T) == 4) {
+              const uint4 a = *reinterpret_cast<const uint4*>(er + e), b = *reinterpret_cast<const uint4*>(er + e + 2);
+              r[0].off = a.x; r[0].w = __uint_as_float(a.y); r[1].off = a.z; r[1].w = __uint_as_float(a.w);
+              r[2].off = b.x; r[2].w = __uint_as_float(b.y); r[3].off = b.z; r[3].w = __uint_as_float(b.w);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) r[u] = er[e + u];
+            }
+            T x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = *reinterpret_cast<const T*>(cb + r[u].off);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc = acc + r[u].w * x[u];
+          }
+          for (; e < cnt; ++e) {
+            const RecEdge<T> r0 = er[e];
+            acc = acc + r0.w * *reinterpret_cast<const T*>(cb + r0.off);
+          }
+          v = node_sum_act<T>(nd, acc);
         } else {
-          acc = agg_neutral<T>(st.agg);
-          for (int e = 0; e < st.count; ++e) acc = agg_combine<T>(st.agg, acc, wt[e0 + e] * cur[srcs[e0 + e]]);
+          T acc;
+          if (nd.agg == AGG_SUM || nd.agg == AGG_MEAN) {  // (mean divides in agg_finish)
+            acc = T(0);
+            for (int e = 0; e < cnt; ++e) acc = acc + er[e].w * *reinterpret_cast<const T*>(cb + er[e].off);
+          } else {
+            acc = agg_neutral<T>(nd.agg);
+            for (int e = 0; e < cnt; ++e)
+              acc = agg_combine<T>(nd.agg, acc, er[e].w * *reinterpret_cast<const T*>(cb + er[e].off));
+          }
+          const T a = agg_finish<T>(nd.agg, acc, cnt);
+          if constexpr (sizeof(T) == 8) v = apply_act(nd.act, fma(nd.resp, a, nd.bias));
+          else v = apply_act(nd.act, fmaf(nd.resp, a, nd.bias));
         }
-        if (st.slot != NO_SLOT) nxt[st.slot] = node_value<T>(st, acc, st.count);
+        if (nd.slot != NO_SLOT) nxt[nd.slot] = v;
       }
       __syncwarp();
       T* tmp = cur; cur = nxt; nxt = tmp;
@@ -169,7 +241,8 @@ int an_rollout(const void* program, int64_t program_stride, int N, int C, int pr
   const ProgLayout L = prog_layout(N, C, O, precision);
   if (L.stride != program_stride) return -3;
   const int slots = max(maxdims_host[0], I);
-  const int max_n = max(maxdims_host[1], 1), max_e = max(C, 1);  // compact edges: at most one per connection
+  // compact edges: at most one per connection, plus one pad record per node
+  const int max_n = max(maxdims_host[1], 1), max_e = max(C + max_n, 1);
   const int wpb = 4;
   const int64_t esz = precision ? 8 : 4;
   const int64_t per = precision ? rollout_warp_bytes<double>(slots, D, O, max_n, max_e)
