@@ -95,8 +95,9 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
  * bounds, so no host-side counts, extents or synchronisation are needed
  * (a transform + forward step can be enqueued ahead or graph-captured).
  * Replaces inference.forward_arrays (inference.py:185-262) for such
- * populations.  plan_ids int32[6 * P] and plan_counts int32[6] are DEVICE
- * scratch owned by the caller; inputs / outputs as an_forward (float32).
+ * populations.  plan_ids int32[6 * P] and plan_counts int32[12] are DEVICE
+ * scratch owned by the caller (counts[6..11]: the class launches' dynamic
+ * task counters, zeroed by the plan); inputs / outputs as an_forward (float32).
  * genome_sq: optional (P,) float32, zeroed by the caller: += the sum of the
  * genome's squared outputs (a fused fitness epilogue; float atomics, so the
  * summation order -- and the last bits -- vary between runs), or NULL. */
@@ -105,7 +106,8 @@ int an_forward_planned(const void* program, int64_t program_stride, int N, int C
                        int64_t input_genome_stride, int64_t P, int B, int I, int O, void* outputs,
                        float* genome_sq, void* stream);
 
-/* The plan step of an_forward_planned alone (diagnostics): plan_counts[c] =
+/* The plan step of an_forward_planned alone (diagnostics; plan_counts
+ * int32[12], [6..11] zeroed): plan_counts[c] =
  * genomes of class c (0..3 tensor-core programs with round16(steps) <= 32, 48,
  * 64, 128; 4 tensor-core programs with > 512 hidden-edge entries; 5 standard
  * programs), plan_ids[c * P + i] their program rows in population order. */

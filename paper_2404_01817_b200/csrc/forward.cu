@@ -920,6 +920,7 @@ struct TcShared {
   uint32_t slot_col[TC_MAX_WG];     // column offset of warpgroup w's slot
   int32_t hdr[2][4];                // n_steps, n_edges, n_groups, genome of buffer b
   uint16_t oslot[2][8];
+  int64_t next_task[2];             // task after task k: next_task[k & 1] (thread 0 writes)
 };
 
 __global__ void __launch_bounds__(TC_NT* TC_MAX_WG, 1)
@@ -928,7 +929,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
               const float* __restrict__ in, int64_t in_gstride,
               int B, int I, int O, int nwg, uint32_t wg_bytes, uint32_t gbuf_bytes, int nbuf, int nb_max,
               float* __restrict__ gsq, float* __restrict__ out,
-              int64_t out_gstride) {
+              int64_t out_gstride, int32_t* __restrict__ task_ctr) {
   // no static shared memory: the dynamic area starts the CTA's shared window,
   // 1024-aligned for the swizzled TMA tiles; the control block is at its end
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -994,14 +995,21 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
   const uint32_t a_addr = smem_u32(wg_area);
   uint32_t tphase = 0, mphase = 0, gphase[2] = {0u, 0u};
 
+  // tasks: the CTA's first is blockIdx.x; later ones come from the launch's
+  // task counter (dynamic: a CTA that drew small genomes takes more of them)
+  // or, without one, every gridDim.x-th
   int k = 0;
-  for (int64_t task = blockIdx.x; task < n_tasks; task += gridDim.x, ++k) {
+  for (int64_t task = blockIdx.x; task < n_tasks; ++k) {
     // two buffers: the next task's genome block is in flight during this one;
     // one buffer (when a second would cost a warpgroup): staged after the barrier
     const int buf = nbuf == 2 ? (k & 1) : 0;
     mbar_wait(smem_u32(&sh.gbar[buf]), gphase[buf]);
     gphase[buf] ^= 1u;
-    if (nbuf == 2 && tid == 0 && task + gridDim.x < n_tasks) issue_stage(task + gridDim.x, buf ^ 1);
+    if (tid == 0) {
+      const int64_t nx = task_ctr ? (int64_t)gridDim.x + atomicAdd(task_ctr, 1) : task + gridDim.x;
+      sh.next_task[k & 1] = nx;
+      if (nbuf == 2 && nx < n_tasks) issue_stage(nx, buf ^ 1);
+    }
     const int run = (int)(task % runs);
     const int t_begin = run * run_tiles, t_end = min(tiles, t_begin + run_tiles);
     const int n_steps = sh.hdr[buf][0], n_edges = sh.hdr[buf][1], n_groups = sh.hdr[buf][2];
@@ -1229,7 +1237,9 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
       if ((tid & 31) == 0) atomicAdd(gsq + gi, sq);
     }
     __syncthreads();  // every warpgroup is done with buffer `buf` before it is restaged
-    if (nbuf == 1 && tid == 0 && task + gridDim.x < n_tasks) issue_stage(task + gridDim.x, 0);
+    const int64_t nx = sh.next_task[k & 1];
+    if (nbuf == 1 && tid == 0 && nx < n_tasks) issue_stage(nx, 0);
+    task = nx;
   }
   tc_fence_before();
   __syncthreads();
@@ -1574,7 +1584,8 @@ inline TcConfig tc_config(int ms, int me, int max_wg) {
 // for small launches) with as many warpgroups as shared memory allows.
 int launch_tc(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, const float* in, int64_t in_gstride,
               int64_t P, int B, int I, int O, const int32_t* maxdims_host, float* out, int64_t out_gstride,
-              int max_wg, cudaStream_t st, const int32_t* count_dev = nullptr, float* gsq = nullptr) {
+              int max_wg, cudaStream_t st, const int32_t* count_dev = nullptr, float* gsq = nullptr,
+              int32_t* task_ctr = nullptr) {
   if (I > TC_K || (I & 3) || (((uintptr_t)in) & 15)) return -8;
   const int ms = max(maxdims_host[1], 1), me = maxdims_host[2];
   const int nb = tc_rows(ms);
@@ -1603,7 +1614,8 @@ int launch_tc(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, cons
   cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (grid == 0) return 0;
   fwd_tc_kernel<<<(unsigned)grid, TC_NT * nwg, smem, st>>>(tmap, prog, L, ids, count_dev, P, in, in_gstride, B, I, O, nwg,
-                                                           wg_bytes, gbuf, nbuf, nb, gsq, out, out_gstride);
+                                                           wg_bytes, gbuf, nbuf, nb, gsq, out, out_gstride,
+                                                           task_ctr);
   TNEAT_CHECK_LAUNCH();
   return 0;
 }
@@ -1661,7 +1673,10 @@ __global__ void __launch_bounds__(1024, 1) plan_tc_kernel(const uint8_t* __restr
     if (cls >= 0) ids[(int64_t)cls * P + wcount[warp][cls] + wpos[cls]] = (int32_t)g;
     __syncthreads();
   }
-  if (tid < TC_NCLASS) counts[tid] = base[tid];
+  if (tid < TC_NCLASS) {
+    counts[tid] = base[tid];
+    counts[TC_NCLASS + tid] = 0;  // the class launch's task counter
+  }
 }
 
 // forward of a whole FMT_TC population from the device plan: the plan kernel,
@@ -1685,7 +1700,7 @@ int launch_planned(const uint8_t* prog, const ProgLayout& L, int N, int C, int32
     if (c < 4 && nb > tc_rows(steps_cap) && c > 0 && tc_class_nb(c - 1) >= tc_rows(steps_cap)) continue;  // empty by construction
     const int32_t md[3] = {nb + 1, nb, c < 4 ? TC_CLASS_EDGES : (int)edge_capacity(N, C)};
     const int r = launch_tc(prog, L, ids + (int64_t)c * P, in, in_gstride, P, B, I, O, md, out, out_gstride, 0, st,
-                            counts + c, gsq);
+                            counts + c, gsq, counts + TC_NCLASS + c);
     if (r) return r;
   }
   // standard programs (genomes the tensor-core format cannot take, cyclic or
@@ -1762,7 +1777,7 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
 
 // FMT_TC populations: forward from a device-side launch plan (no host-known
 // launch sizes; see include/tneat.h).  plan_ids: int32[6 * P] and
-// plan_counts: int32[6] scratch owned by the caller.
+// plan_counts: int32[12] scratch owned by the caller ([6..11]: task counters).
 int an_forward_planned(const void* program, int64_t program_stride, int N, int C, int precision, int32_t* plan_ids,
                        int32_t* plan_counts, const void* inputs, int64_t input_genome_stride, int64_t P, int B, int I,
                        int O, void* outputs, float* genome_sq, void* stream) {

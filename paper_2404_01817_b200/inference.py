@@ -449,13 +449,14 @@ TC_NCLASS = 6  # device launch-plan classes (csrc/forward.cu plan_tc_kernel)
 
 
 def _tc_plan_buffers(stacked: StackedNetworks, device) -> tuple[torch.Tensor, torch.Tensor]:
-    """Scratch of the device-side launch plan (ids int32[6P], counts int32[6]),
+    """Scratch of the device-side launch plan (ids int32[6P]; counts int32[12]:
+    6 class counts, then the class launches' dynamic task counters),
     allocated once per StackedNetworks; the plan itself is rebuilt on the
     device by every forward (no host read-back)."""
     bufs = stacked._cache.get("tcplan")
     if bufs is None:
         bufs = (torch.empty((TC_NCLASS * max(1, stacked.size),), dtype=torch.int32, device=device),
-                torch.empty((TC_NCLASS,), dtype=torch.int32, device=device))
+                torch.empty((2 * TC_NCLASS,), dtype=torch.int32, device=device))
         stacked._cache["tcplan"] = bufs
     return bufs
 
@@ -468,7 +469,7 @@ def tc_plan_counts(stacked: StackedNetworks) -> np.ndarray:
     ids, counts = _tc_plan_buffers(stacked, stacked.program.device)
     _native.call("an_plan_tc", ptr(stacked.program), stacked.stride, stacked.size, ptr(ids), ptr(counts),
                  stream_handle())
-    return counts.cpu().numpy()
+    return counts[:TC_NCLASS].cpu().numpy()
 
 
 def _tc_plan(stacked: StackedNetworks) -> tuple[list, list]:
