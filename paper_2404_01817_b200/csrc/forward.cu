@@ -1345,7 +1345,8 @@ __global__ void fwd_warp_kernel(const uint8_t* __restrict__ prog, ProgLayout L, 
     // then the remainder added one by one
     const uint16_t sl = os[0];
     auto term = [&](int b) {
-      const double y = (double)vals[(int64_t)sl * bchunk + b];
+      // (an errored genome's program has no output slot: NaN; the host raises)
+      const double y = sl != NO_SLOT ? (double)vals[(int64_t)sl * bchunk + b] : __longlong_as_double(0x7ff8000000000000ll);
       const double t = fit_kind == FIT_XOR ? (double)(((b >> 1) ^ b) & 1) : targets[b];
       return (y - t) * (y - t);
     };

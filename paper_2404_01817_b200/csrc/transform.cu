@@ -40,6 +40,7 @@ template <> struct KeyTraits<false> {
   using E = uint64_t;
   using G = uint64_t;
   using Succ = uint16_t;
+  using Idx = int32_t;  // CSR starts (<= C)
   static constexpr int DSH = 48, SSH = 32;
   static constexpr uint32_t FM = 0xFFFF;
   static constexpr G GMAX = ~0ull;
@@ -60,6 +61,7 @@ template <> struct KeyTraits<true> {
   using E = uint32_t;
   using G = uint32_t;
   using Succ = uint8_t;
+  using Idx = int16_t;  // CSR starts (<= C <= 16383)
   static constexpr int DSH = 24, SSH = 16;
   static constexpr uint32_t FM = 0xFF;
   static constexpr G GMAX = ~0u;
@@ -82,22 +84,22 @@ template <typename KT>
 struct WarpSmem {
   using E = typename KT::E;
   using G = typename KT::G;
-  uint64_t* skey;     // [Npad]   (key << 16 | row), sorted
+  uint64_t* skey;     // [Npad]   (key << 16 | row), sorted; dead from Kahn on
   E* ekey;            // [Cpad]   edge keys, sorted (CSR by destination)
   E* ekey2;           // [C]      unsorted staging for the counting sort
-  G* gkey;            // [Npad]   step sort keys
+  G* gkey;            // [pow2(N - I)] step sort keys
   int32_t* indeg;     // [N]
   int32_t* outdeg;    // [N]
-  int32_t* in_start;  // [N+1]    CSR by destination into ekey
-  int32_t* su_start;  // [N+1]    CSR by source into succ
+  typename KT::Idx* in_start;  // [N+1]    CSR by destination into ekey
+  typename KT::Idx* su_start;  // [N+1]    CSR by source into succ (TC programs: the step's weight exponent)
   int32_t* lvl;       // [N]      topological level
   int32_t* last_grp;  // [N+1]    last group that reads the node (level starts during Kahn)
   typename KT::Succ* succ;  // [C] destination rows, CSR by source
   uint16_t* order;    // [N]
   uint16_t* slot_of;  // [N]
-  uint16_t* step_row; // [N]
-  uint16_t* grp_of;   // [N]
-  GroupRec* grp;      // [N]
+  uint16_t* step_row; // [N - I]
+  uint16_t* grp_of;   // [N - I]
+  GroupRec* grp;      // [N - I]  (steps are non-input nodes)
   uint8_t* flags;     // [N]
   uint8_t* needed;    // [N]
   uint8_t* used;      // [N]
@@ -112,10 +114,12 @@ __host__ __device__ inline int next_pow2(int x) {
 }
 
 template <bool kCarve, typename KT>
-__host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, WarpSmem<KT>* s) {
+__host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, int I, WarpSmem<KT>* s) {
   using E = typename KT::E;
   using G = typename KT::G;
+  using Idx = typename KT::Idx;
   const int Npad = next_pow2(N), Cpad = next_pow2(C);
+  const int S = N - I > 1 ? N - I : 1, Spad = next_pow2(S);  // steps are non-input nodes
   const int W = (N + 31) / 32, WS = (N + 2 + 31) / 32;
   int64_t o = 0;
   auto take = [&](int64_t bytes, int64_t al) {
@@ -124,19 +128,20 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, Warp
     o += bytes;
     return at;
   };
-  const int64_t a_skey = take(8ll * Npad, 8), a_ekey = take((int64_t)sizeof(E) * Cpad, 8);
-  // union: ekey2 (edge staging, dead once the CSR is built) shares memory with
-  // the arrays that are first written after Kahn (gkey, grp, last_grp,
-  // step_row, grp_of)
+  const int64_t a_ekey = take((int64_t)sizeof(E) * Cpad, 8);
+  // union: the key table and ekey2 (edge staging), both dead once the CSR is
+  // built (the io rows are looked up before Kahn), share memory with the
+  // arrays first written by Kahn and after it (gkey, grp, last_grp, step_row,
+  // grp_of)
   const int64_t a_union = take(0, 16);
-  const int64_t a_gkey = take((int64_t)sizeof(G) * Npad, 8), a_grp = take(16ll * N, 16);
+  const int64_t a_gkey = take((int64_t)sizeof(G) * Spad, 8), a_grp = take(16ll * S, 16);
   const int64_t a_last = take(4ll * (N + 1), 4);  // also the level starts of the level-synchronous Kahn
-  const int64_t a_srow = take(2ll * N, 2), a_grpof = take(2ll * N, 2);
-  const int64_t a_ekey2 = a_union;
-  const int64_t e2 = (int64_t)sizeof(E) * (C > 0 ? C : 1);
-  o = a_union + (o - a_union > e2 ? o - a_union : e2);
+  const int64_t a_srow = take(2ll * S, 2), a_grpof = take(2ll * S, 2);
+  const int64_t a_skey = a_union, a_ekey2 = align_up(a_union + 8ll * Npad, 8);
+  const int64_t front = a_ekey2 + (int64_t)sizeof(E) * (C > 0 ? C : 1) - a_union;
+  o = a_union + (o - a_union > front ? o - a_union : front);
   const int64_t a_indeg = take(4ll * N, 4), a_outdeg = take(4ll * N, 4);
-  const int64_t a_in = take(4ll * (N + 1), 4), a_su = take(4ll * (N + 1), 4);
+  const int64_t a_in = take((int64_t)sizeof(Idx) * (N + 1), 4), a_su = take((int64_t)sizeof(Idx) * (N + 1), 4);
   const int64_t a_lvl = take(4ll * N, 4);
   const int64_t a_succ = take((int64_t)sizeof(typename KT::Succ) * C, 2), a_order = take(2ll * N, 2),
                 a_slot = take(2ll * N, 2);
@@ -149,8 +154,8 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, Warp
     s->gkey = (G*)(base + a_gkey);
     s->indeg = (int32_t*)(base + a_indeg);
     s->outdeg = (int32_t*)(base + a_outdeg);
-    s->in_start = (int32_t*)(base + a_in);
-    s->su_start = (int32_t*)(base + a_su);
+    s->in_start = (Idx*)(base + a_in);
+    s->su_start = (Idx*)(base + a_su);
     s->lvl = (int32_t*)(base + a_lvl);
     s->last_grp = (int32_t*)(base + a_last);
     s->grp = (GroupRec*)(base + a_grp);
@@ -168,9 +173,9 @@ __host__ __device__ inline int64_t layout_warp(uint8_t* base, int N, int C, Warp
   return align_up(o, 16);
 }
 
-__host__ inline int64_t warp_smem_bytes(int N, int C) {
-  if (small_keys(N, C)) return layout_warp<false, KeyTraits<true>>(nullptr, N, C, nullptr);
-  return layout_warp<false, KeyTraits<false>>(nullptr, N, C, nullptr);
+__host__ inline int64_t warp_smem_bytes(int N, int C, int I) {
+  if (small_keys(N, C)) return layout_warp<false, KeyTraits<true>>(nullptr, N, C, I, nullptr);
+  return layout_warp<false, KeyTraits<false>>(nullptr, N, C, I, nullptr);
 }
 
 // ascending bitonic sort of n (power of two, >= 32) values, one warp
@@ -192,7 +197,8 @@ __device__ void warp_bitonic_sort(K* a, int n) {
 }
 
 // exclusive scan of cnt[0..n) into out[0..n]; out[n] = total. One warp.
-__device__ void warp_exclusive_scan(const int32_t* cnt, int32_t* out, int n) {
+template <typename OutT>
+__device__ void warp_exclusive_scan(const int32_t* cnt, OutT* out, int n) {
   const int lane = threadIdx.x & 31;
   int32_t carry = 0;
   for (int base = 0; base < n; base += 32) {
@@ -204,10 +210,10 @@ __device__ void warp_exclusive_scan(const int32_t* cnt, int32_t* out, int n) {
       const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
       if (lane >= d) x += y;
     }
-    if (i < n) out[i] = carry + x - v;
+    if (i < n) out[i] = (OutT)(carry + x - v);
     carry += __shfl_sync(0xffffffffu, x, 31);
   }
-  if (lane == 0) out[n] = carry;
+  if (lane == 0) out[n] = (OutT)carry;
   __syncwarp();
 }
 
@@ -219,7 +225,7 @@ __device__ void warp_exclusive_scan(const int32_t* cnt, int32_t* out, int n) {
 // position (the CSR by source).
 template <typename KT>
 __device__ void stable_scatter(const typename KT::E* in, typename KT::E* out, int n, int shift,
-                               const int32_t* start, int32_t* cursor, typename KT::Succ* succ) {
+                               const typename KT::Idx* start, int32_t* cursor, typename KT::Succ* succ) {
   const int lane = threadIdx.x & 31;
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
@@ -270,7 +276,7 @@ __device__ inline int warp_first_set(const uint32_t* words, int nw) {
 }
 
 template <typename T, bool SMALL>
-__global__ void transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
+__global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
                                  int64_t P, int N, int C, int I, int O, int mode, int prune, bool tc,
                                  int64_t wsmem, uint8_t* __restrict__ prog, ProgLayout L,
                                  int16_t* __restrict__ order_out, int16_t* __restrict__ conn_rows,
@@ -283,7 +289,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
   if (g >= P) return;
   using KT = KeyTraits<SMALL>;
   WarpSmem<KT> s;
-  layout_warp<true, KT>(smem + warp * wsmem, N, C, &s);
+  layout_warp<true, KT>(smem + warp * wsmem, N, C, I, &s);
   const int Npad = next_pow2(N);
   const double* gn = nodes + g * (int64_t)N * 5;
   const double* gc = conns + g * (int64_t)C * 4;
@@ -444,8 +450,8 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
       }
       __syncwarp();
       for (int i = lane; i < carry; i += 32) s.ekey[i] = s.ekey2[i];
-      for (int r = lane; r < N; r += 32) s.in_start[r] = s.outdeg[r];
-      if (lane == 0) s.in_start[N] = carry;
+      for (int r = lane; r < N; r += 32) s.in_start[r] = (typename KT::Idx)s.outdeg[r];
+      if (lane == 0) s.in_start[N] = (typename KT::Idx)carry;
     }
   }
   for (int r = lane; r < N; r += 32) s.lvl[r] = 0;
@@ -454,6 +460,18 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
 #if defined(XSTOP) && XSTOP == 2
   if (lane < 32) return;
 #endif
+  // ---- io rows (the key table is dead from Kahn on: its memory is reused) ----
+  // output rows park in the program's output-slot area; they become slots at the end
+  uint8_t* gp = prog + g * L.stride;
+  uint16_t* out_slot = (uint16_t*)(gp + L.off_out);
+  for (int k = lane; k < io; k += 32) {
+    const int r = lookup_row(s.skey, Npad, (uint64_t)k);
+    if (r < 0) status |= ST_MISSING_IO;
+    if (io_rows) io_rows[g * io + k] = r;
+    if (k >= I) out_slot[k - I] = r >= 0 ? (uint16_t)r : NO_SLOT;
+  }
+  __syncwarp();
+
   // ---- Kahn, smallest ready row first (inference.py:127-141) + levels ---------
   const int W = (N + 31) / 32;
   for (int w = 0; w < W; ++w) {
@@ -539,16 +557,11 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     for (int i = lane; i < N; i += 32)
       order_out[g * N + i] = i < n_order ? (int16_t)s.order[i] : (int16_t)-1;
   }
-  for (int k = lane; k < io; k += 32) {
-    const int r = lookup_row(s.skey, Npad, (uint64_t)k);
-    if (r < 0) status |= ST_MISSING_IO;
-    if (io_rows) io_rows[g * io + k] = r;
-  }
   status = __reduce_or_sync(0xffffffffu, status);
 
-  uint8_t* gp = prog + g * L.stride;
   ProgHeader* hdr = (ProgHeader*)gp;
   if ((status & ~ST_CYCLIC) || ((status & ST_CYCLIC) && !recurrent)) {
+    for (int o = lane; o < O; o += 32) out_slot[o] = NO_SLOT;
     if (lane == 0) {
       ProgHeader h{0, 0, I, n_order, status, n_live, mode, 0};
       *hdr = h;
@@ -648,7 +661,7 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
         // weights / cf and response * cf must stay normal floats (the exponent is
         // kept in su_start, free for TC programs from here on)
         const int ewx = mw != 0.0 ? ilogb(mw) : 12;
-        s.su_start[r] = ewx;
+        s.su_start[r] = (typename KT::Idx)ewx;
         const double up = ldexp(1.0, 12 - ewx), dn = ldexp(1.0, ewx - 12);
         if (!(hmax * up < 0x1p100)) bad = 1;
         if (hmin != INFINITY) {
@@ -1023,10 +1036,10 @@ __global__ void transform_kernel(const double* __restrict__ nodes, const double*
     for (int k = n_emit + lane; k < tc_rows(n_emit); k += 32)
       for (int q = 0; q < 12; ++q) *(uint4*)(bp + tc_offset(k, 8 * q)) = make_uint4(0, 0, 0, 0);
   }
-  uint16_t* out_slot = (uint16_t*)(gp + L.off_out);
-  for (int o = lane; o < O; o += 32) {
-    const int r = lookup_row(s.skey, Npad, (uint64_t)(I + o));
-    out_slot[o] = r >= 0 ? s.slot_of[r] : NO_SLOT;
+  for (int k = lane; k < io; k += 32) {  // output rows -> slots (the lane that parked them)
+    if (k < I) continue;
+    const uint16_t r = out_slot[k - I];
+    out_slot[k - I] = r != NO_SLOT ? s.slot_of[r] : NO_SLOT;
   }
   TNEAT_DCHECK(e_total <= edge_capacity(N, C), "program edge entries within capacity", e_total, edge_capacity(N, C));
   TNEAT_DCHECK(!tc_ok || L.off_tc + tb.bytes <= L.off_in, "tc block within its area", tb.bytes, L.off_in - L.off_tc);
@@ -1067,7 +1080,7 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
   if (P == 0) return 0;  // empty population: nothing to read or write
   if (!nodes || !program || !maxdims || (C > 0 && !conns)) return -2;
   const int Cc = C > 0 ? C : 1;
-  const int64_t ws = warp_smem_bytes(N, Cc);
+  const int64_t ws = warp_smem_bytes(N, Cc, I);
   if (ws > 200 * 1024) return -4;  // genome capacity too large for one warp's shared memory
 #ifndef TNEAT_TR_WPB
 #define TNEAT_TR_WPB 1  // one genome-warp per CTA: its shared memory is released as soon as it finishes
