@@ -241,8 +241,10 @@ int an_rollout(const void* program, int64_t program_stride, int N, int C, int pr
   const ProgLayout L = prog_layout(N, C, O, precision);
   if (L.stride != program_stride) return -3;
   const int slots = max(maxdims_host[0], I);
-  // compact edges: at most one per connection, plus one pad record per node
-  const int max_n = max(maxdims_host[1], 1), max_e = max(C + max_n, 1);
+  // compact edges: at most one per connection, plus one pad record per node;
+  // maxdims[2] (edge entries: every recurrent step its own group, padded to 8)
+  // bounds the padded lists as well and is usually tighter
+  const int max_n = max(maxdims_host[1], 1), max_e = max(min(C + max_n, maxdims_host[2]), 1);
   const int wpb = 4;
   const int64_t esz = precision ? 8 : 4;
   const int64_t per = precision ? rollout_warp_bytes<double>(slots, D, O, max_n, max_e)
