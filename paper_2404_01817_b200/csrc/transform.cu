@@ -260,6 +260,33 @@ __device__ inline int lookup_row(const uint64_t* skey, int Npad, uint64_t key) {
   return (e != U64_MAX && (e >> 16) == key) ? (int)(e & 0xFFFF) : -1;
 }
 
+// both endpoints of a connection at once: two independent search chains
+__device__ inline void lookup_rows2(const uint64_t* skey, int Npad, uint64_t ka, uint64_t kb, int& ra, int& rb) {
+  const uint64_t sa = ka << 16, sb = kb << 16;
+  int pa = 0, pb = 0;
+  for (int step = Npad >> 1; step > 0; step >>= 1) {
+    pa = skey[pa + step - 1] < sa ? pa + step : pa;
+    pb = skey[pb + step - 1] < sb ? pb + step : pb;
+  }
+  const uint64_t ea = skey[pa], eb = skey[pb];
+  ra = (ea != U64_MAX && (ea >> 16) == ka) ? (int)(ea & 0xFFFF) : -1;
+  rb = (eb != U64_MAX && (eb >> 16) == kb) ? (int)(eb & 0xFFFF) : -1;
+}
+
+// one connection row's in key, out key and enabled flag (16-byte key load
+// when the population is 16-byte aligned; rows are 32 bytes)
+__device__ __forceinline__ void load_conn(const double* gc, int c, bool vec, double& ik, double& ok, double& en) {
+  if (vec) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(gc + (int64_t)c * 4));
+    ik = a.x;
+    ok = a.y;
+  } else {
+    ik = __ldg(gc + (int64_t)c * 4);
+    ok = __ldg(gc + (int64_t)c * 4 + 1);
+  }
+  en = __ldg(gc + (int64_t)c * 4 + 2);
+}
+
 __device__ inline bool key_ok(double k) {
   return k >= 0.0 && k < 140737488355328.0 /* 2^47 */ && k == floor(k);
 }
@@ -306,7 +333,9 @@ __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const dou
     uint64_t packed = U64_MAX;
     if (r < N) {
       uint8_t f = 0;
-      const double k = gn[(int64_t)r * 5];
+      // the three fields in flight together: one round trip per row
+      const double k = __ldg(gn + (int64_t)r * 5), gv = __ldg(gn + (int64_t)r * 5 + 3),
+                   av = __ldg(gn + (int64_t)r * 5 + 4);
       if (!isnan(k)) {
         if (!key_ok(k)) status |= ST_BAD_KEY;
         const uint64_t ki = (uint64_t)k;
@@ -314,7 +343,6 @@ __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const dou
         f = F_LIVE | (ki < (uint64_t)I ? F_INPUT : 0) | (ki >= (uint64_t)I && ki < (uint64_t)io ? F_OUTPUT : 0);
         ++n_live;
         if (ki >= (uint64_t)I) {  // the reference evaluates every live non-input node (pruned ones too)
-          const double av = gn[(int64_t)r * 5 + 4], gv = gn[(int64_t)r * 5 + 3];
           if (!(av >= 0.0 && av < ACT_COUNT && av == floor(av))) status |= ST_BAD_ACT;
           if (!(gv >= 0.0 && gv < AGG_COUNT && gv == floor(gv))) status |= ST_BAD_AGG;
           if (av == (double)ACT_TANH && gv == (double)AGG_SUM) f |= F_TANH_SUM;  // read by the group pass
@@ -344,21 +372,34 @@ __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const dou
 #endif
   // ---- conns: endpoint rows, enabled mask, compacted edge keys ----------------
   int n_en = 0;
+  // rows software-pipelined: the next iteration's row is in flight during this
+  // one's searches (a genome's transform is latency-bound when few genomes
+  // share an SM, e.g. one GPU's shard of a multi-GPU population)
+  const bool vec = ((uint64_t)gc & 15) == 0;
+  double nik = 0.0, nok = 0.0, nen = 0.0;
+  if (lane < C) load_conn(gc, lane, vec, nik, nok, nen);
   for (int base = 0; base < C; base += 32) {
     const int c = base + lane;
     bool en = false;
     int sr = -1, dr = -1;
+    const double ik = nik, ok = nok, env = nen;
+    if (c + 32 < C) load_conn(gc, c + 32, vec, nik, nok, nen);
     if (c < C) {
-      const double ik = gc[(int64_t)c * 4 + 0];
       if (!isnan(ik)) {
-        const double ok = gc[(int64_t)c * 4 + 1];
         if (!key_ok(ik) || !key_ok(ok)) {
           status |= ST_BAD_KEY;
         } else {
-          sr = (io_fast && ik < (double)io) ? (int)ik : lookup_row(s.skey, Npad, (uint64_t)ik);
-          dr = (io_fast && ok < (double)io) ? (int)ok : lookup_row(s.skey, Npad, (uint64_t)ok);
+          const bool fs = io_fast && ik < (double)io, fd = io_fast && ok < (double)io;
+          if (fs && fd) {
+            sr = (int)ik;
+            dr = (int)ok;
+          } else {
+            lookup_rows2(s.skey, Npad, (uint64_t)ik, (uint64_t)ok, sr, dr);
+            if (fs) sr = (int)ik;
+            if (fd) dr = (int)ok;
+          }
           if (sr < 0 || dr < 0) status |= ST_DANGLING;
-          else en = gc[(int64_t)c * 4 + 2] == 1.0;
+          else en = env == 1.0;
         }
       }
       if (conn_rows) {
