@@ -938,6 +938,9 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
   const int bar_id = 1 + wg;
   uint8_t* const wg_area = smem + (uint32_t)wg * wg_bytes;
   uint8_t* const gbuf0 = smem + (uint32_t)nwg * wg_bytes;
+  // the next class launch of a device plan may take SMs as this grid's CTAs
+  // exit (programmatic dependent launch; a no-op otherwise)
+  asm volatile("griddepcontrol.launch_dependents;");
   if (count_dev) P = __ldg(count_dev);  // device launch plan: this class's genome count
   const uint32_t slot_cols = 4u * (uint32_t)nb_max;
   const uint32_t n_slots = 512u / slot_cols;
@@ -1247,6 +1250,10 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_in, const uint8_t* __rest
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  // launched early behind the previous class launch: complete only after it
+  // (so every later stream operation follows the whole chain); immediate for
+  // a normal launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -1586,7 +1593,7 @@ inline TcConfig tc_config(int ms, int me, int max_wg) {
 int launch_tc(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, const float* in, int64_t in_gstride,
               int64_t P, int B, int I, int O, const int32_t* maxdims_host, float* out, int64_t out_gstride,
               int max_wg, cudaStream_t st, const int32_t* count_dev = nullptr, float* gsq = nullptr,
-              int32_t* task_ctr = nullptr) {
+              int32_t* task_ctr = nullptr, bool pdl = false) {
   if (I > TC_K || (I & 3) || (((uintptr_t)in) & 15)) return -8;
   const int ms = max(maxdims_host[1], 1), me = maxdims_host[2];
   const int nb = tc_rows(ms);
@@ -1614,9 +1621,19 @@ int launch_tc(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, cons
     return -9;
   cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (grid == 0) return 0;
-  fwd_tc_kernel<<<(unsigned)grid, TC_NT * nwg, smem, st>>>(tmap, prog, L, ids, count_dev, P, in, in_gstride, B, I, O, nwg,
-                                                           wg_bytes, gbuf, nbuf, nb, gsq, out, out_gstride,
-                                                           task_ctr);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)grid);
+  lc.blockDim = dim3((unsigned)(TC_NT * nwg));
+  lc.dynamicSmemBytes = (size_t)smem;
+  lc.stream = st;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = la;
+  lc.numAttrs = pdl ? 1 : 0;
+  const cudaError_t le = cudaLaunchKernelEx(&lc, fwd_tc_kernel, tmap, prog, L, ids, count_dev, P, in, in_gstride, B, I,
+                                            O, nwg, wg_bytes, gbuf, nbuf, nb, gsq, out, out_gstride, task_ctr);
+  if (le != cudaSuccess) return -100 - (int)le;
   TNEAT_CHECK_LAUNCH();
   return 0;
 }
@@ -1696,13 +1713,19 @@ int launch_planned(const uint8_t* prog, const ProgLayout& L, int N, int C, int32
   }
   plan_tc_kernel<<<1, 1024, 0, st>>>(prog, L.stride, P, ids, counts);
   TNEAT_CHECK_LAUNCH();
+  // class launches after the first are programmatic dependent launches: each
+  // one's CTAs start on SMs the previous launch's drain frees (the launches are
+  // independent: disjoint genomes, their own task counters; the plan they
+  // read completed before the first one started)
+  bool first = true;
   for (int c = 0; c < 5; ++c) {
     const int nb = c < 4 ? tc_class_nb(c) : tc_rows(steps_cap);
     if (c < 4 && nb > tc_rows(steps_cap) && c > 0 && tc_class_nb(c - 1) >= tc_rows(steps_cap)) continue;  // empty by construction
     const int32_t md[3] = {nb + 1, nb, c < 4 ? TC_CLASS_EDGES : (int)edge_capacity(N, C)};
     const int r = launch_tc(prog, L, ids + (int64_t)c * P, in, in_gstride, P, B, I, O, md, out, out_gstride, 0, st,
-                            counts + c, gsq, counts + TC_NCLASS + c);
+                            counts + c, gsq, counts + TC_NCLASS + c, !first);
     if (r) return r;
+    first = false;
   }
   // standard programs (genomes the tensor-core format cannot take, cyclic or
   // invalid genomes): capacity-sized tile launch
