@@ -95,8 +95,8 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
  * bounds, so no host-side counts, extents or synchronisation are needed
  * (a transform + forward step can be enqueued ahead or graph-captured).
  * Replaces inference.forward_arrays (inference.py:185-262) for such
- * populations.  plan_ids int32[6 * P] and plan_counts int32[12] are DEVICE
- * scratch owned by the caller (counts[6..11]: the class launches' dynamic
+ * populations.  plan_ids int32[7 * P] and plan_counts int32[14] are DEVICE
+ * scratch owned by the caller (counts[7..13]: the class launches' dynamic
  * task counters, zeroed by the plan); inputs / outputs as an_forward (float32).
  * genome_sq: optional (P,) float32, zeroed by the caller: += the sum of the
  * genome's squared outputs (a fused fitness epilogue; float atomics, so the
@@ -107,10 +107,11 @@ int an_forward_planned(const void* program, int64_t program_stride, int N, int C
                        float* genome_sq, void* stream);
 
 /* The plan step of an_forward_planned alone (diagnostics; plan_counts
- * int32[12], [6..11] zeroed): plan_counts[c] =
- * genomes of class c (0..3 tensor-core programs with round16(steps) <= 32, 48,
- * 64, 128; 4 tensor-core programs with > 512 hidden-edge entries; 5 standard
- * programs), plan_ids[c * P + i] their program rows in population order. */
+ * int32[14], [7..13] zeroed): plan_counts[c] =
+ * genomes of class c (0..4 tensor-core programs with round16(steps) <= 32, 48,
+ * 64, 96, 128; 5 tensor-core programs with > 512 hidden-edge entries; 6
+ * standard programs), plan_ids[c * P + i] their program rows in population
+ * order. */
 int an_plan_tc(const void* program, int64_t program_stride, int64_t P, int32_t* plan_ids, int32_t* plan_counts,
                void* stream);
 

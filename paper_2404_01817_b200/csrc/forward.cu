@@ -1641,15 +1641,16 @@ int launch_tc(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, cons
 // ---------------------------------------------------------------------------
 // device-side launch plan of an FMT_TC population (no host read-back)
 // ---------------------------------------------------------------------------
-// Class of a genome: 0..3 tensor-core programs by MMA width (round16(steps) <=
-// 32, 48, 64, 128) whose hidden-edge entries fit the class buffer; 4 tensor-core
-// programs with more entries (buffer sized by the capacity); 5 standard
+// Class of a genome: 0..4 tensor-core programs by MMA width (round16(steps) <=
+// 32, 48, 64, 96, 128: 4, 4, 3, 2, 1 warpgroups per CTA) whose hidden-edge
+// entries fit the class buffer; 5 tensor-core programs with more entries
+// (buffer sized by the capacity); 6 standard
 // programs (the tile kernel with capacity-sized shared memory).  One CTA, a
 // deterministic block scan per class: ids[c * P + i] = i-th genome of class c
 // in population order, counts[c].
-constexpr int TC_NCLASS = 6;
+constexpr int TC_NCLASS = 7;
 constexpr int TC_CLASS_EDGES = 512;
-__host__ __device__ inline int tc_class_nb(int c) { return c == 0 ? 32 : c == 1 ? 48 : c == 2 ? 64 : 128; }
+__host__ __device__ inline int tc_class_nb(int c) { return c == 0 ? 32 : c == 1 ? 48 : c == 2 ? 64 : c == 3 ? 96 : 128; }
 
 __global__ void __launch_bounds__(1024, 1) plan_tc_kernel(const uint8_t* __restrict__ prog, int64_t stride, int64_t P,
                                                           int32_t* __restrict__ ids, int32_t* __restrict__ counts) {
@@ -1664,10 +1665,10 @@ __global__ void __launch_bounds__(1024, 1) plan_tc_kernel(const uint8_t* __restr
     if (g < P) {
       const ProgHeader h = *reinterpret_cast<const ProgHeader*>(prog + g * stride);
       if (h.mode != MODE_TC) {
-        cls = 5;
+        cls = 6;
       } else {
         const int nb = tc_rows(h.n_steps);
-        cls = h.n_edges > TC_CLASS_EDGES ? 4 : nb <= 32 ? 0 : nb <= 48 ? 1 : nb <= 64 ? 2 : 3;
+        cls = h.n_edges > TC_CLASS_EDGES ? 5 : nb <= 32 ? 0 : nb <= 48 ? 1 : nb <= 64 ? 2 : nb <= 96 ? 3 : 4;
       }
     }
     int wpos[TC_NCLASS];
@@ -1718,10 +1719,10 @@ int launch_planned(const uint8_t* prog, const ProgLayout& L, int N, int C, int32
   // independent: disjoint genomes, their own task counters; the plan they
   // read completed before the first one started)
   bool first = true;
-  for (int c = 0; c < 5; ++c) {
-    const int nb = c < 4 ? tc_class_nb(c) : tc_rows(steps_cap);
-    if (c < 4 && nb > tc_rows(steps_cap) && c > 0 && tc_class_nb(c - 1) >= tc_rows(steps_cap)) continue;  // empty by construction
-    const int32_t md[3] = {nb + 1, nb, c < 4 ? TC_CLASS_EDGES : (int)edge_capacity(N, C)};
+  for (int c = 0; c < TC_NCLASS - 1; ++c) {
+    const int nb = c < 5 ? tc_class_nb(c) : tc_rows(steps_cap);
+    if (c < 5 && nb > tc_rows(steps_cap) && c > 0 && tc_class_nb(c - 1) >= tc_rows(steps_cap)) continue;  // empty by construction
+    const int32_t md[3] = {nb + 1, nb, c < 5 ? TC_CLASS_EDGES : (int)edge_capacity(N, C)};
     const int r = launch_tc(prog, L, ids + (int64_t)c * P, in, in_gstride, P, B, I, O, md, out, out_gstride, 0, st,
                             counts + c, gsq, counts + TC_NCLASS + c, !first);
     if (r) return r;
@@ -1730,8 +1731,8 @@ int launch_planned(const uint8_t* prog, const ProgLayout& L, int N, int C, int32
   // standard programs (genomes the tensor-core format cannot take, cyclic or
   // invalid genomes): capacity-sized tile launch
   const int32_t md[3] = {N + 2, N, (int)edge_capacity(N, C)};
-  return launch_tile<float, 2, 64>(prog, L, ids + 5 * P, in, in_gstride, P, B, I, O, md, out, out_gstride, 4, st,
-                                   counts + 5, gsq);
+  return launch_tile<float, 2, 64>(prog, L, ids + 6 * P, in, in_gstride, P, B, I, O, md, out, out_gstride, 4, st,
+                                   counts + 6, gsq);
 }
 
 }  // namespace tneat
@@ -1800,8 +1801,8 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
 }
 
 // FMT_TC populations: forward from a device-side launch plan (no host-known
-// launch sizes; see include/tneat.h).  plan_ids: int32[6 * P] and
-// plan_counts: int32[12] scratch owned by the caller ([6..11]: task counters).
+// launch sizes; see include/tneat.h).  plan_ids: int32[7 * P] and
+// plan_counts: int32[14] scratch owned by the caller ([7..13]: task counters).
 int an_forward_planned(const void* program, int64_t program_stride, int N, int C, int precision, int32_t* plan_ids,
                        int32_t* plan_counts, const void* inputs, int64_t input_genome_stride, int64_t P, int B, int I,
                        int O, void* outputs, float* genome_sq, void* stream) {

@@ -445,12 +445,12 @@ def _bucket_plan(stacked: StackedNetworks, variant: int, subset: np.ndarray | No
     return plan
 
 
-TC_NCLASS = 6  # device launch-plan classes (csrc/forward.cu plan_tc_kernel)
+TC_NCLASS = 7  # device launch-plan classes (csrc/forward.cu plan_tc_kernel)
 
 
 def _tc_plan_buffers(stacked: StackedNetworks, device) -> tuple[torch.Tensor, torch.Tensor]:
-    """Scratch of the device-side launch plan (ids int32[6P]; counts int32[12]:
-    6 class counts, then the class launches' dynamic task counters),
+    """Scratch of the device-side launch plan (ids int32[7P]; counts int32[14]:
+    7 class counts, then the class launches' dynamic task counters),
     allocated once per StackedNetworks; the plan itself is rebuilt on the
     device by every forward (no host read-back)."""
     bufs = stacked._cache.get("tcplan")
@@ -462,9 +462,9 @@ def _tc_plan_buffers(stacked: StackedNetworks, device) -> tuple[torch.Tensor, to
 
 
 def tc_plan_counts(stacked: StackedNetworks) -> np.ndarray:
-    """Genomes per device-plan class of an FMT_TC population (classes 0-3:
-    tensor-core programs by MMA width 32/48/64/128, 4: tensor-core programs
-    with more hidden-edge entries than the class buffer, 5: standard programs).
+    """Genomes per device-plan class of an FMT_TC population (classes 0-4:
+    tensor-core programs by MMA width 32/48/64/96/128, 5: tensor-core programs
+    with more hidden-edge entries than the class buffer, 6: standard programs).
     Diagnostics and tests; the forward does not need it."""
     ids, counts = _tc_plan_buffers(stacked, stacked.program.device)
     _native.call("an_plan_tc", ptr(stacked.program), stacked.stride, stacked.size, ptr(ids), ptr(counts),

@@ -56,7 +56,7 @@ def _plan(tn, st):
 def test_bench_plan_has_every_bucket(bench_run):
     tn, st, *_ = bench_run
     plan, counts = _plan(tn, st)
-    assert counts[5] == 0  # every tanh/sum genome takes the tensor-core format
+    assert counts[6] == 0  # every tanh/sum genome takes the tensor-core format
     assert counts.sum() == POP
     assert (counts[:3] > 0).all(), counts  # MMA-width classes 32 / 48 / 64 are all launched
 

@@ -373,7 +373,7 @@ def test_device_plan_classes_cover_population(tn):
     assert np.array_equal(np.sort(got), np.arange(st.size))
     for c in range(tn.inference.TC_NCLASS):
         assert np.all(np.diff(ids[c, :counts[c]]) > 0)
-    assert counts[5] == int((st._cache["modes"] != tn.inference.MODE_TC).sum())
+    assert counts[6] == int((st._cache["modes"] != tn.inference.MODE_TC).sum())
     x = torch.randn(st.size, 600, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(10))
     st._cache["tc_host_plan"] = False
     planned = tn.forward_device(st, x)

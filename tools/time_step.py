@@ -17,6 +17,7 @@ ap.add_argument("--reps", type=int, default=4)
 ap.add_argument("--layout", default="auto")
 ap.add_argument("--lib", default=None, help="alternative libtneat.so build (tuning experiments)")
 ap.add_argument("--fwd-reps", type=int, default=10)
+ap.add_argument("--prune", type=int, default=1)
 a = ap.parse_args()
 if a.lib:
     from paper_2404_01817_b200 import _native
@@ -28,7 +29,7 @@ out = torch.empty((a.pop, 4096, 8), device="cuda")
 for rep in range(a.reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    st, _ = tn.transform_arrays(nodes, conns, 32, 8, sync=False, layout=a.layout)
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8, sync=False, layout=a.layout, prune=bool(a.prune))
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     tn.finalize_transform(st)
@@ -58,7 +59,7 @@ tvs = []
 for _ in range(a.fwd_reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    tn.transform_arrays(nodes, conns, 32, 8, sync=False, layout=a.layout)
+    tn.transform_arrays(nodes, conns, 32, 8, sync=False, layout=a.layout, prune=bool(a.prune))
     e1.record()
     torch.cuda.synchronize()
     tvs.append(e0.elapsed_time(e1))
