@@ -313,9 +313,9 @@ def secondary(dev) -> dict:
 
     timed("config1_xor", lambda: bc.bench_xor(types.SimpleNamespace(seed=0, gens=100, no_cpu=False)))
     timed("config3_generation_1m", lambda: bc.bench_generation(
-        types.SimpleNamespace(pop=1_000_000, gens=3, ref_pop=0)))
+        types.SimpleNamespace(pop=1_000_000, gens=5, ref_pop=0)))
     timed("config3_generation_100k", lambda: bc.bench_generation(
-        types.SimpleNamespace(pop=100_000, gens=3, ref_pop=100_000)))
+        types.SimpleNamespace(pop=100_000, gens=5, ref_pop=100_000)))
     timed("config4_hyperneat", lambda: bc.bench_hyperneat(types.SimpleNamespace(pop=10_000, no_cpu=False)))
     timed("config5_recurrent", lambda: bc.bench_recurrent(
         types.SimpleNamespace(pop=10_000, steps=1000, sweeps=[5], no_cpu=False)))

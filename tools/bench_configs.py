@@ -125,7 +125,10 @@ def bench_generation(a):
                "scaled_s_per_gen_at_pop": rdt * a.pop / a.ref_pop, "threads": 1,
                "note": "generation 0 from init_state; scaled linearly to the GPU run's population"}
     out = {"config": f"3: generation pop {a.pop} 50/100 (XOR, threshold 1.0)", "init_s": t_init,
-           "phases": phases, "gen_per_s": 1.0 / last["gen_s"],
+           "phases": phases,
+           # steady state: the median of the last (up to) three generations (the
+           # first ones carry allocator growth; speciation time varies by run)
+           "gen_per_s": 1.0 / float(np.median([p["gen_s"] for p in phases[-3:]])),
            "reproduce_GBps_min_traffic": 3 * a.pop * genome_bytes / last["reproduce_s"] / 1e9,
            "genome_bytes": genome_bytes, "gpu_mem_GB": torch.cuda.max_memory_allocated() / 1e9,
            "cpu_reference": ref}
