@@ -380,3 +380,26 @@ def test_device_plan_classes_cover_population(tn):
     st._cache["tc_host_plan"] = True
     hosted = tn.forward_device(st, x)
     assert torch.equal(planned, hosted)
+
+
+def test_unpruned_wide_classes_match_oracle(tn):
+    """Unpruned programs of genomes with up to 120 hidden nodes fill every device-plan
+    class: MMA widths 32 / 48 / 64, the 96 class (two warpgroups sharing one TMEM
+    slot), the 128 class (one warpgroup per CTA) and standard programs (> 128 steps).
+    Genomes of each populated class match the oracle at 1e-5."""
+    import torch
+    from oracle import arrayneat_oracle as orc
+    nodes, conns = orc.synthetic_population(160, 160, 512, 32, 8, seed=95)
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8, prune=False)
+    counts = tn.inference.tc_plan_counts(st)
+    assert (counts[[0, 1, 2, 3, 4]] > 0).all(), counts
+    ids = st._cache["tcplan"][0].view(tn.inference.TC_NCLASS, -1).cpu().numpy()
+    x = torch.randn(st.size, 384, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(12))
+    out = tn.forward_device(st, x).cpu().numpy()
+    xs = x.cpu().numpy().astype(np.float64)
+    for c in range(tn.inference.TC_NCLASS):
+        for p in ids[c, :counts[c]][:4]:
+            tr = orc.transform_genome(nodes[p], conns[p], 32, 8)
+            ref = orc.forward_genome(nodes[p], tr, xs[p])
+            err = np.max(np.abs(out[p] - ref) / np.maximum(1.0, np.abs(ref)))
+            assert err <= 1e-5, (c, int(p), float(err))
