@@ -403,3 +403,29 @@ def test_unpruned_wide_classes_match_oracle(tn):
             ref = orc.forward_genome(nodes[p], tr, xs[p])
             err = np.max(np.abs(out[p] - ref) / np.maximum(1.0, np.abs(ref)))
             assert err <= 1e-5, (c, int(p), float(err))
+
+
+def test_back_to_back_steps_keep_stream_order(tn):
+    """Transform + device-planned forward steps enqueued back to back with no host
+    synchronisation (the bench's step; the class launches are programmatic
+    dependent launches and the caching allocator hands the next transform the
+    memory of the previous programs) give exactly the isolated results."""
+    import torch
+    from oracle import arrayneat_oracle as orc
+    pops = [orc.synthetic_population(300, 128, 512, 32, 8, seed=s) for s in (96, 97)]
+    x = torch.randn(300, 512, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(13))
+    refs = []
+    for nodes, conns in pops:
+        st, _ = tn.transform_arrays(nodes, conns, 32, 8)
+        refs.append(tn.forward_device(st, x).clone())
+        del st
+    torch.cuda.synchronize()
+    nd = [(torch.from_numpy(n).cuda(), torch.from_numpy(c).cuda()) for n, c in pops]
+    outs = []
+    for k in range(6):
+        st, _ = tn.transform_arrays(*nd[k % 2], 32, 8, sync=False)
+        outs.append(tn.forward_device(st, x))
+        del st
+    torch.cuda.synchronize()
+    for k, o in enumerate(outs):
+        assert torch.equal(o, refs[k % 2]), k
