@@ -107,11 +107,11 @@ int an_forward_planned(const void* program, int64_t program_stride, int N, int C
                        float* genome_sq, void* stream);
 
 /* The plan step of an_forward_planned alone (diagnostics; plan_counts
- * int32[14], [7..13] zeroed): plan_counts[c] =
- * genomes of class c (0..4 tensor-core programs with round16(steps) <= 32, 48,
- * 64, 96, 128; 5 tensor-core programs with > 512 hidden-edge entries; 6
- * standard programs), plan_ids[c * P + i] their program rows in population
- * order. */
+ * int32[14], zeroed on the stream first): plan_counts[c] = genomes of class c
+ * (0..4 tensor-core programs with round16(steps) <= 32, 48, 64, 96, 128; 5
+ * tensor-core programs with > 512 hidden-edge entries; 6 standard programs),
+ * plan_ids[c * P + i] their program rows (in no particular order: the class
+ * launches hand genomes out dynamically). */
 int an_plan_tc(const void* program, int64_t program_stride, int64_t P, int32_t* plan_ids, int32_t* plan_counts,
                void* stream);
 

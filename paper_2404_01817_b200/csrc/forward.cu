@@ -1641,60 +1641,44 @@ int launch_tc(const uint8_t* prog, const ProgLayout& L, const int32_t* ids, cons
 // ---------------------------------------------------------------------------
 // device-side launch plan of an FMT_TC population (no host read-back)
 // ---------------------------------------------------------------------------
-// Class of a genome: 0..4 tensor-core programs by MMA width (round16(steps) <=
+// Class of a genome (plan_tc_kernel): 0..4 tensor-core programs by MMA width (round16(steps) <=
 // 32, 48, 64, 96, 128: 4, 4, 3, 2, 1 warpgroups per CTA) whose hidden-edge
 // entries fit the class buffer; 5 tensor-core programs with more entries
 // (buffer sized by the capacity); 6 standard
-// programs (the tile kernel with capacity-sized shared memory).  One CTA, a
-// deterministic block scan per class: ids[c * P + i] = i-th genome of class c
-// in population order, counts[c].
+// programs (the tile kernel with capacity-sized shared memory).  A thread per
+// genome, positions claimed per warp with one atomic per class: ids[c * P + i]
+// = the class's genomes (in no particular order), counts[c].
 constexpr int TC_NCLASS = 7;
 constexpr int TC_CLASS_EDGES = 512;
 __host__ __device__ inline int tc_class_nb(int c) { return c == 0 ? 32 : c == 1 ? 48 : c == 2 ? 64 : c == 3 ? 96 : 128; }
 
-__global__ void __launch_bounds__(1024, 1) plan_tc_kernel(const uint8_t* __restrict__ prog, int64_t stride, int64_t P,
-                                                          int32_t* __restrict__ ids, int32_t* __restrict__ counts) {
-  __shared__ int wcount[32][TC_NCLASS];
-  __shared__ int base[TC_NCLASS];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < TC_NCLASS) base[tid] = 0;
-  __syncthreads();
-  for (int64_t chunk = 0; chunk < P; chunk += 1024) {
-    const int64_t g = chunk + tid;
-    int cls = -1;
-    if (g < P) {
-      const ProgHeader h = *reinterpret_cast<const ProgHeader*>(prog + g * stride);
-      if (h.mode != MODE_TC) {
-        cls = 6;
-      } else {
-        const int nb = tc_rows(h.n_steps);
-        cls = h.n_edges > TC_CLASS_EDGES ? 5 : nb <= 32 ? 0 : nb <= 48 ? 1 : nb <= 64 ? 2 : nb <= 96 ? 3 : 4;
-      }
+__global__ void __launch_bounds__(1024) plan_tc_kernel(const uint8_t* __restrict__ prog, int64_t stride, int64_t P,
+                                                       int32_t* __restrict__ ids, int32_t* __restrict__ counts) {
+  // one genome per thread over as many CTAs as needed; each warp claims its
+  // positions per class with one atomic (counts zeroed on the stream first).
+  // The order inside a class is the order the warps reach the counters: the
+  // class launches hand tasks out dynamically, so no order is needed.
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int cls = -1;
+  if (g < P) {
+    const ProgHeader h = *reinterpret_cast<const ProgHeader*>(prog + g * stride);
+    if (h.mode != MODE_TC) {
+      cls = 6;
+    } else {
+      const int nb = tc_rows(h.n_steps);
+      cls = h.n_edges > TC_CLASS_EDGES ? 5 : nb <= 32 ? 0 : nb <= 48 ? 1 : nb <= 64 ? 2 : nb <= 96 ? 3 : 4;
     }
-    int wpos[TC_NCLASS];
-#pragma unroll
-    for (int c = 0; c < TC_NCLASS; ++c) {
-      const unsigned m = __ballot_sync(0xffffffffu, cls == c);
-      wpos[c] = __popc(m & ((1u << lane) - 1));
-      if (lane == 0) wcount[warp][c] = __popc(m);
-    }
-    __syncthreads();
-    if (tid < TC_NCLASS) {  // exclusive scan over the warps, per class
-      int run = base[tid];
-      for (int w = 0; w < 32; ++w) {
-        const int t = wcount[w][tid];
-        wcount[w][tid] = run;
-        run += t;
-      }
-      base[tid] = run;
-    }
-    __syncthreads();
-    if (cls >= 0) ids[(int64_t)cls * P + wcount[warp][cls] + wpos[cls]] = (int32_t)g;
-    __syncthreads();
   }
-  if (tid < TC_NCLASS) {
-    counts[tid] = base[tid];
-    counts[TC_NCLASS + tid] = 0;  // the class launch's task counter
+#pragma unroll
+  for (int c = 0; c < TC_NCLASS; ++c) {
+    const unsigned m = __ballot_sync(0xffffffffu, cls == c);
+    if (!m) continue;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(counts + c, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (cls == c) ids[(int64_t)c * P + base + __popc(m & ((1u << lane) - 1))] = (int32_t)g;
   }
 }
 
@@ -1712,7 +1696,9 @@ int launch_planned(const uint8_t* prog, const ProgLayout& L, int N, int C, int32
     const int64_t tile_smem = align_up(32ll * N + 8ll * edge_capacity(N, C) + 16, 16) + (int64_t)(N + 2) * 130 * 4;
     if (tile_smem > 227 * 1024) return -6;
   }
-  plan_tc_kernel<<<1, 1024, 0, st>>>(prog, L.stride, P, ids, counts);
+  // class counts and the class launches' task counters start at zero
+  if (cudaMemsetAsync(counts, 0, 2 * TC_NCLASS * sizeof(int32_t), st) != cudaSuccess) return -100 - (int)cudaGetLastError();
+  plan_tc_kernel<<<(unsigned)((P + 1023) / 1024), 1024, 0, st>>>(prog, L.stride, P, ids, counts);
   TNEAT_CHECK_LAUNCH();
   // class launches after the first are programmatic dependent launches: each
   // one's CTAs start on SMs the previous launch's drain frees (the launches are
@@ -1823,8 +1809,12 @@ int an_plan_tc(const void* program, int64_t program_stride, int64_t P, int32_t* 
   if (P < 0) return -1;
   if (!program || !plan_ids || !plan_counts) return -2;
   if (P > 0x7FFFFFFF / TC_NCLASS) return -5;
-  plan_tc_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>((const uint8_t*)program, program_stride, P, plan_ids,
-                                                         plan_counts);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(plan_counts, 0, 2 * TC_NCLASS * sizeof(int32_t), st) != cudaSuccess)
+    return -100 - (int)cudaGetLastError();
+  if (P == 0) return 0;
+  plan_tc_kernel<<<(unsigned)((P + 1023) / 1024), 1024, 0, st>>>((const uint8_t*)program, program_stride, P,
+                                                                  plan_ids, plan_counts);
   TNEAT_CHECK_LAUNCH();
   return 0;
 }
