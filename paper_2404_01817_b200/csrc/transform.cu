@@ -302,6 +302,10 @@ __device__ inline int warp_first_set(const uint32_t* words, int nw) {
   return (int)wmin * 32 + __ffs(words[wmin]) - 1;
 }
 
+// TNEAT_DIAG_TR_STOP=k (diagnostic builds, tools/build_variant.py): the kernel
+// returns at phase boundary k (6 entry, 7 nodes, 1 connections, 2 CSR, 3 Kahn,
+// 8 io outputs, 4 pruning + TC eligibility, 5 steps / groups / slots) --
+// tools/time_transform.py times the cumulative phases
 template <typename T, bool SMALL>
 __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
                                  int64_t P, int N, int C, int I, int O, int mode, int prune, bool tc,
@@ -324,8 +328,8 @@ __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const dou
   const bool recurrent = mode == 1;
   int status = 0;
 
-#if defined(XSTOP) && XSTOP == 6
-  if (lane < 32) return;
+#if defined(TNEAT_DIAG_TR_STOP) && TNEAT_DIAG_TR_STOP == 6  // diagnostic builds only: phase split
+  return;
 #endif
   // ---- nodes: live mask, key table ------------------------------------------
   int n_live = 0;
@@ -367,8 +371,8 @@ __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const dou
   __syncwarp();
   warp_bitonic_sort(s.skey, Npad);
 
-#if defined(XSTOP) && XSTOP == 7
-  if (lane < 32) return;
+#if defined(TNEAT_DIAG_TR_STOP) && TNEAT_DIAG_TR_STOP == 7  // diagnostic builds only: phase split
+  return;
 #endif
   // ---- conns: endpoint rows, enabled mask, compacted edge keys ----------------
   int n_en = 0;
@@ -416,8 +420,8 @@ __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const dou
   }
   __syncwarp();
 
-#if defined(XSTOP) && XSTOP == 1
-  if (lane < 32) return;
+#if defined(TNEAT_DIAG_TR_STOP) && TNEAT_DIAG_TR_STOP == 1  // diagnostic builds only: phase split
+  return;
 #endif
   // ---- counting sort by destination, then by source inside each bucket; CSR by
   // destination (in_start) and by source (su_start/succ) ------------------------
@@ -498,8 +502,8 @@ __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const dou
   for (int r = lane; r < N; r += 32) s.lvl[r] = 0;
   __syncwarp();
 
-#if defined(XSTOP) && XSTOP == 2
-  if (lane < 32) return;
+#if defined(TNEAT_DIAG_TR_STOP) && TNEAT_DIAG_TR_STOP == 2  // diagnostic builds only: phase split
+  return;
 #endif
   // ---- io rows (the key table is dead from Kahn on: its memory is reused) ----
   // output rows park in the program's output-slot area; they become slots at the end
@@ -590,8 +594,8 @@ __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const dou
   }
   if (n_order < n_live) status |= ST_CYCLIC;
 
-#if defined(XSTOP) && XSTOP == 3
-  if (lane < 32) return;
+#if defined(TNEAT_DIAG_TR_STOP) && TNEAT_DIAG_TR_STOP == 3  // diagnostic builds only: phase split
+  return;
 #endif
   // ---- order / io rows outputs -----------------------------------------------
   if (order_out) {
@@ -728,8 +732,8 @@ __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const dou
   }
   __syncwarp();
 
-#if defined(XSTOP) && XSTOP == 4
-  if (lane < 32) return;
+#if defined(TNEAT_DIAG_TR_STOP) && TNEAT_DIAG_TR_STOP == 4  // diagnostic builds only: phase split
+  return;
 #endif
   // ---- steps: emitted nodes sorted by (level, class, -count, position) --------
   // feed-forward: positions in the Kahn order; recurrent: rows (all nodes are
@@ -915,8 +919,8 @@ __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const dou
     for (int k = lane; k <= n_emit; k += 32) in_start[k] = (uint16_t)s.last_grp[k];
   }
 
-#if defined(XSTOP) && XSTOP == 5
-  if (lane < 32) return;
+#if defined(TNEAT_DIAG_TR_STOP) && TNEAT_DIAG_TR_STOP == 5  // diagnostic builds only: phase split
+  return;
 #endif
   // ---- write groups, steps and interleaved edge lists --------------------------
   // (TC programs: into the staged block, common.cuh tc_block)
