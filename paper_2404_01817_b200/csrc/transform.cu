@@ -303,8 +303,9 @@ __device__ inline int warp_first_set(const uint32_t* words, int nw) {
 }
 
 // TNEAT_DIAG_TR_STOP=k (diagnostic builds, tools/build_variant.py): the kernel
-// returns at phase boundary k (6 entry, 7 nodes, 1 connections, 2 CSR, 3 Kahn,
-// 8 io outputs, 4 pruning + TC eligibility, 5 steps / groups / slots) --
+// returns before phase k's successor (6 entry, 7 nodes, 1 connections, 2 CSR
+// and repeated pairs, 3 io rows + Kahn, 4 pruning + TC eligibility, 5 steps /
+// groups / slots; the full kernel adds the program writes) --
 // tools/time_transform.py times the cumulative phases
 template <typename T, bool SMALL>
 __global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
