@@ -372,6 +372,16 @@ def gather_fitness(fit_local, fit_all, world: int) -> None:
         fit_all.copy_(fit_local)
 
 
+def _tc_launches(max_nodes: int) -> int:
+    """Kernel launches of one device-planned forward (csrc/forward.cu
+    launch_planned): the plan, one per MMA-width class a genome of this
+    capacity can reach (32/48/64/96/128), the oversized class, the standard one."""
+    cap = (min(max_nodes, 128) + 15) // 16 * 16
+    nbs = (32, 48, 64, 96, 128)
+    width = sum(1 for c, nb in enumerate(nbs) if not (c > 0 and nb > cap and nbs[c - 1] >= cap))
+    return 1 + width + 1 + 1
+
+
 def _local_device() -> int:
     """This rank's GPU.  TNEAT_BENCH_SHARE_GPU=1 (tests of the multi-rank path on
     a one-GPU box, with TNEAT_BENCH_BACKEND=gloo) puts every rank on cuda:0."""
@@ -508,7 +518,7 @@ def run_ours(args, rank: int, world: int) -> None:
     tn.finalize_transform(st)
     prog_bytes = _program_bytes(tn, st)
     if st.precision & tn.inference.FMT_TC:
-        launches_fwd = 1 + 6  # plan kernel + 5 tensor-core class launches + the standard-program launch
+        launches_fwd = _tc_launches(MAXN)
         kernel = "fwd_tc_kernel (+ plan_tc_kernel, fwd_tile_kernel for standard programs)"
     else:
         launches_fwd = len(tn.inference._bucket_plan(st, (args.variant & 0xF) or 5))
