@@ -76,7 +76,8 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
  *   genome_ids  optional (P,) int32 DEVICE list of program rows to evaluate
  *            (NULL = rows 0..P-1); inputs/outputs are addressed by program row,
  *            so a launch per slot-count bucket raises occupancy
- *   variant  0 auto, 1/3 = tile kernel 1 input/thread (128/64 threads),
+ *   variant  0 auto (B >= 192: 5 for fp32 programs, 1 for fp64; B >= 96: 3;
+ *            else 8), 1/3 = tile kernel 1 input/thread (128/64 threads),
  *            2/5 = 2 inputs/thread (128/64 threads), 4 = 4 inputs/thread,
  *            8 = warp-per-genome kernel (small B), 11 = tensor-core kernel
  *            (FMT_TC programs whose header mode is 2; persistent, one CTA per

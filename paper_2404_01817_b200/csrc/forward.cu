@@ -1757,7 +1757,7 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
   // an FMT_TC population holds tensor-core programs the standard kernels cannot
   // read: they take explicitly listed standard-program genomes only
   if ((precision & FMT_TC) && !genome_ids) return -7;
-  if (variant == 0) variant = B >= 192 ? 5 : (B >= 96 ? 3 : 8);
+  if (variant == 0) variant = B >= 192 ? ((precision & FMT_F64) ? 1 : 5) : (B >= 96 ? 3 : 8);  // fp64: one sample per thread
   if (variant == 8) {
     if (genome_ids) return -7;
     if (precision & FMT_F64)
@@ -1772,6 +1772,8 @@ int an_forward(const void* program, int64_t program_stride, int N, int C, int pr
     double* out = (double*)outputs;
     if (variant == 2 || variant == 5)
       return launch_tile<double, 2, 64>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
+    if (variant == 3)  // half the samples per CTA: fp64 value rows are twice as wide
+      return launch_tile<double, 1, 64>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
     return launch_tile<double, 1, 128>(pg, L, ids, in, input_genome_stride, P, B, I, O, maxdims_host, out, ogs, tpc, st);
   }
   const float* in = (const float*)inputs;

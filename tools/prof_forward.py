@@ -16,13 +16,15 @@ ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--batch", type=int, default=4096)
 ap.add_argument("--layout", default="auto")
+ap.add_argument("--precision", default="f32")
 a = ap.parse_args()
 n, c = synthetic_population(a.pop, 128, 512, 32, 8, seed=20261018)
 nodes, conns = torch.from_numpy(n).cuda(), torch.from_numpy(c).cuda()
-x = torch.randn((a.pop, a.batch, 32), device="cuda")
-out = torch.empty((a.pop, a.batch, 8), device="cuda")
+dt = torch.float64 if a.precision == "f64" else torch.float32
+x = torch.randn((a.pop, a.batch, 32), device="cuda", dtype=dt)
+out = torch.empty((a.pop, a.batch, 8), device="cuda", dtype=dt)
 for _ in range(a.steps):
-    st, _ = tn.transform_arrays(nodes, conns, 32, 8, layout=a.layout)
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8, layout=a.layout, precision=a.precision)
     tn.forward_device(st, x, out, variant=a.variant)
 torch.cuda.synchronize()
 print("maxdims", st.maxdims)

@@ -18,18 +18,20 @@ ap.add_argument("--layout", default="auto")
 ap.add_argument("--lib", default=None, help="alternative libtneat.so build (tuning experiments)")
 ap.add_argument("--fwd-reps", type=int, default=10)
 ap.add_argument("--prune", type=int, default=1)
+ap.add_argument("--precision", default="f32")
 a = ap.parse_args()
 if a.lib:
     from paper_2404_01817_b200 import _native
     _native.LIB_PATH = os.path.abspath(a.lib)
 n, c = synthetic_population(a.pop, 128, 512, 32, 8, seed=20261018)
 nodes, conns = torch.from_numpy(n).cuda(), torch.from_numpy(c).cuda()
-x = torch.randn((a.pop, 4096, 32), device="cuda")
-out = torch.empty((a.pop, 4096, 8), device="cuda")
+dt = torch.float64 if a.precision == "f64" else torch.float32
+x = torch.randn((a.pop, 4096, 32), device="cuda", dtype=dt)
+out = torch.empty((a.pop, 4096, 8), device="cuda", dtype=dt)
 for rep in range(a.reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    st, _ = tn.transform_arrays(nodes, conns, 32, 8, sync=False, layout=a.layout, prune=bool(a.prune))
+    st, _ = tn.transform_arrays(nodes, conns, 32, 8, sync=False, layout=a.layout, prune=bool(a.prune), precision=a.precision)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     tn.finalize_transform(st)
@@ -59,7 +61,7 @@ tvs = []
 for _ in range(a.fwd_reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    tn.transform_arrays(nodes, conns, 32, 8, sync=False, layout=a.layout, prune=bool(a.prune))
+    tn.transform_arrays(nodes, conns, 32, 8, sync=False, layout=a.layout, prune=bool(a.prune), precision=a.precision)
     e1.record()
     torch.cuda.synchronize()
     tvs.append(e0.elapsed_time(e1))
