@@ -254,8 +254,10 @@ template <typename T> __device__ __forceinline__ T agg_neutral(int agg) {
 template <typename T> __device__ __forceinline__ T agg_combine(int agg, T acc, T x) {
   switch (agg) {
     case AGG_PRODUCT: return acc * x;
-    case AGG_MAX: return acc > x ? acc : x;
-    case AGG_MIN: return acc < x ? acc : x;
+    // numpy's maximum / minimum (functions.py:37 reduces with np.max): a NaN on
+    // either side wins, ties keep the accumulator
+    case AGG_MAX: return (acc >= x || acc != acc) ? acc : x;
+    case AGG_MIN: return (acc <= x || acc != acc) ? acc : x;
     default: return acc + x;
   }
 }

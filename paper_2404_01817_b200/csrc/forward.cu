@@ -359,8 +359,10 @@ __device__ __forceinline__ void run_sum_group_f64(const GroupRec& gr, const Edge
 template <typename T, int AGG>
 __device__ __forceinline__ T agg_step(T acc, T x) {
   if constexpr (AGG == AGG_PRODUCT) return acc * x;
-  else if constexpr (AGG == AGG_MAX) return acc > x ? acc : x;
-  else if constexpr (AGG == AGG_MIN) return acc < x ? acc : x;
+  // numpy's maximum / minimum (the reference's max reduction): a NaN on either
+  // side wins, ties keep the accumulator
+  else if constexpr (AGG == AGG_MAX) return (acc >= x || acc != acc) ? acc : x;
+  else if constexpr (AGG == AGG_MIN) return (acc <= x || acc != acc) ? acc : x;
   else return acc + x;
 }
 
