@@ -221,7 +221,7 @@ __device__ __forceinline__ float sigmoid_fast(float x) {
 __device__ __forceinline__ float step_act(float kx, float ca, float cb, bool relu, float pre) {
   const float sg = rcp_approx(1.0f + ex2_approx(kx * pre));
   const float smooth = fmaf(ca, sg, cb);
-  const float lin = relu ? fmaxf(pre, 0.0f) : pre;
+  const float lin = relu ? ((pre >= 0.0f || pre != pre) ? pre : 0.0f) : pre;  // np.maximum(x, 0): NaN stays
   return kx != 0.0f ? smooth : lin;
 }
 
@@ -229,7 +229,7 @@ __device__ __forceinline__ float apply_act(int code, float x) {
   switch (code) {
     case ACT_TANH: return tanh_fast(x);
     case ACT_SIGMOID: return sigmoid_fast(x);
-    case ACT_RELU: return fmaxf(x, 0.0f);
+    case ACT_RELU: return (x >= 0.0f || x != x) ? x : 0.0f;  // np.maximum(x, 0.0) (functions.py:30): NaN stays
     default: return x;
   }
 }
@@ -237,7 +237,7 @@ __device__ __forceinline__ double apply_act(int code, double x) {
   switch (code) {
     case ACT_TANH: return tanh(x);
     case ACT_SIGMOID: return x >= 0.0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
-    case ACT_RELU: return fmax(x, 0.0);
+    case ACT_RELU: return (x >= 0.0 || x != x) ? x : 0.0;
     default: return x;
   }
 }

@@ -139,26 +139,26 @@ except Exception as e:
 def test_max_min_propagate_nan_like_numpy(tn, precision, batch):
     """max / min aggregations propagate a NaN term wherever it sits, as the
     reference's np.max does (functions.py:37): 0 * inf is NaN, and a later,
-    larger finite term must not replace it (warp kernel at B=1, tile kernel at
-    B=256)."""
+    larger finite term must not replace it; relu of a NaN pre-activation stays
+    NaN (np.maximum, functions.py:30).  Warp kernel at B=1, tile kernel at B=256."""
     import torch
     from oracle import arrayneat_oracle as orc
     nan = np.nan
-    nodes = np.full((2, 4, 5), nan)
-    conns = np.full((2, 4, 4), nan)
-    for g, agg in enumerate((2, 4)):  # max, min
+    nodes = np.full((3, 4, 5), nan)
+    conns = np.full((3, 4, 4), nan)
+    for g, (agg, act) in enumerate(((2, 0), (4, 0), (0, 3))):  # max, min; sum -> relu (np.maximum(x, 0))
         nodes[g, 0] = [0, 0.0, 1.0, 0, 0]
         nodes[g, 1] = [1, 0.0, 1.0, 0, 0]
-        nodes[g, 2] = [2, 0.0, 1.0, agg, 0]  # output, identity activation
+        nodes[g, 2] = [2, 0.0, 1.0, agg, act]  # the output
         conns[g, 0] = [0, 2, 1.0, 0.0]       # 0 * inf -> NaN, the first term
         conns[g, 1] = [1, 2, 1.0, 1.0]
     st, _ = tn.transform_arrays(nodes, conns, 2, 1, precision=precision)
     dt = torch.float64 if precision == "f64" else torch.float32
-    x = torch.zeros((2, batch, 2), dtype=dt)
+    x = torch.zeros((3, batch, 2), dtype=dt)
     x[:, :, 0] = float("inf")
     x[:, :, 1] = torch.linspace(-3, 3, batch, dtype=dt)
     out = tn.forward_device(st, x.cuda()).cpu().numpy()
-    for g in range(2):
+    for g in range(3):
         ref = orc.forward_genome(nodes[g], orc.transform_genome(nodes[g], conns[g], 2, 1),
                                  x[g].numpy().astype(np.float64))
         assert np.all(np.isnan(ref)) and np.all(np.isnan(out[g])), (g, out[g][:4])
