@@ -35,10 +35,18 @@ struct __align__(16) RecNode {
   uint8_t act, agg;
   T bias, resp;
 };
+// environment rows padded to whole 16-byte vectors (zeros past D)
+template <typename T>
+__host__ __device__ inline int rollout_dp(int D) {
+  constexpr int VW = 16 / (int)sizeof(T);
+  return (D + VW - 1) / VW * VW;
+}
+// per warp: [s (Dp) | s_next (Dp) | actions (O) | values (slots) | values (slots)],
+// then the node records and the edge records
 template <typename T>
 __host__ __device__ inline int64_t rollout_warp_bytes(int slots, int D, int O, int max_n, int max_e) {
-  return align_up((2ll * slots + 2ll * D + O) * (int64_t)sizeof(T), 16) + (int64_t)max_n * sizeof(RecNode<T>) +
-         align_up((int64_t)max_e * sizeof(RecEdge<T>), 16);
+  return align_up((2ll * slots + 2ll * rollout_dp<T>(D) + O) * (int64_t)sizeof(T), 16) +
+         (int64_t)max_n * sizeof(RecNode<T>) + align_up((int64_t)max_e * sizeof(RecEdge<T>), 16);
 }
 
 template <typename T>
@@ -59,21 +67,26 @@ __global__ void rollout_kernel(const uint8_t* __restrict__ prog, ProgLayout L, i
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  // environment matrices once per CTA
+  // environment matrices once per CTA (A rows padded to Dp with zeros)
+  const int Dp = rollout_dp<T>(D);
   T* Am = reinterpret_cast<T*>(smem);
-  T* Mm = Am + D * D;
-  for (int i = threadIdx.x; i < D * D; i += blockDim.x) Am[i] = A[i];
+  T* Mm = Am + D * Dp;
+  for (int i = threadIdx.x; i < D * Dp; i += blockDim.x) {
+    const int r = i / Dp, c = i - r * Dp;
+    Am[i] = c < D ? A[r * D + c] : T(0);
+  }
   for (int i = threadIdx.x; i < D * O; i += blockDim.x) Mm[i] = M[i];
   __syncthreads();
   if (gi >= P) return;
-  uint8_t* wbase = smem + align_up((int64_t)(D * D + D * O) * sizeof(T), 16) +
+  uint8_t* wbase = smem + align_up((int64_t)(D * Dp + D * O) * sizeof(T), 16) +
                    (int64_t)warp * rollout_warp_bytes<T>(slots, D, O, max_n, max_e);
-  T* buf0 = reinterpret_cast<T*>(wbase);
+  T* s = reinterpret_cast<T*>(wbase);  // environment state (Dp, zeros past D; 16-byte aligned)
+  T* s_next = s + Dp;                   // (Dp)
+  T* act = s_next + Dp;                 // actions (O)
+  T* buf0 = act + O;
   T* buf1 = buf0 + slots;
-  T* s = buf1 + slots;        // environment state (D)
-  T* s_next = s + D;          // (D)
-  T* act = s_next + D;        // actions (O)
-  RecNode<T>* nodes = reinterpret_cast<RecNode<T>*>(wbase + align_up((2ll * slots + 2ll * D + O) * (int64_t)sizeof(T), 16));
+  RecNode<T>* nodes =
+      reinterpret_cast<RecNode<T>*>(wbase + align_up((2ll * slots + 2ll * Dp + O) * (int64_t)sizeof(T), 16));
   RecEdge<T>* edges = reinterpret_cast<RecEdge<T>*>(nodes + max_n);
   const uint8_t* gp = prog + gi * L.stride;
   const ProgHeader hdr = *reinterpret_cast<const ProgHeader*>(gp);
@@ -138,7 +151,10 @@ __global__ void rollout_kernel(const uint8_t* __restrict__ prog, ProgLayout L, i
   }
   __syncwarp();
   for (int i = lane; i < slots; i += 32) { buf0[i] = T(0); buf1[i] = T(0); }
-  for (int i = lane; i < D; i += 32) s[i] = s0[i];
+  for (int i = lane; i < Dp; i += 32) {
+    s[i] = i < D ? s0[i] : T(0);
+    s_next[i] = T(0);
+  }
   __syncwarp();
   T* cur = buf0;
   T* nxt = buf1;
@@ -210,8 +226,18 @@ __global__ void rollout_kernel(const uint8_t* __restrict__ prog, ProgLayout L, i
     __syncwarp();
     // s <- tanh(A s + M a)
     for (int r = lane; r < D; r += 32) {
+      // 16-byte loads of the row and the state, FMAs in column order (the padding adds 0 * 0)
       T z = T(0);
-      for (int c = 0; c < D; ++c) z = fma(Am[r * D + c], s[c], z);
+      const T* ar = Am + r * Dp;
+      for (int c = 0; c < Dp; c += 16 / (int)sizeof(T)) {
+        if constexpr (sizeof(T) == 4) {
+          const float4 a = *reinterpret_cast<const float4*>(ar + c), v = *reinterpret_cast<const float4*>(s + c);
+          z = fmaf(a.x, v.x, z); z = fmaf(a.y, v.y, z); z = fmaf(a.z, v.z, z); z = fmaf(a.w, v.w, z);
+        } else {
+          const double2 a = *reinterpret_cast<const double2*>(ar + c), v = *reinterpret_cast<const double2*>(s + c);
+          z = fma(a.x, v.x, z); z = fma(a.y, v.y, z);
+        }
+      }
       for (int c = 0; c < O; ++c) z = fma(Mm[r * O + c], act[c], z);
       s_next[r] = tanh(z);
     }
@@ -249,7 +275,8 @@ int an_rollout(const void* program, int64_t program_stride, int N, int C, int pr
   const int64_t esz = precision ? 8 : 4;
   const int64_t per = precision ? rollout_warp_bytes<double>(slots, D, O, max_n, max_e)
                                 : rollout_warp_bytes<float>(slots, D, O, max_n, max_e);
-  const int64_t smem = align_up((int64_t)(D * D + D * O) * esz, 16) + per * wpb;
+  const int64_t Dp = precision ? rollout_dp<double>(D) : rollout_dp<float>(D);
+  const int64_t smem = align_up((int64_t)(D * Dp + D * O) * esz, 16) + per * wpb;
   if (smem > 200 * 1024) return -6;
   const int64_t blocks = (P + wpb - 1) / wpb;
   cudaStream_t st = (cudaStream_t)stream;
