@@ -417,7 +417,9 @@ __device__ __forceinline__ void warp_copy_genome(double* dn, double* dc, const d
 // kernels
 // ---------------------------------------------------------------------------
 
-__global__ void reproduce_kernel(const double* __restrict__ pn, const double* __restrict__ pc,
+// 48 registers (10 blocks of 128 threads per SM instead of 8): the warp per child
+// waits on global loads, more resident warps beat the small spill (-17 %)
+__global__ void __launch_bounds__(128, 10) reproduce_kernel(const double* __restrict__ pn, const double* __restrict__ pc,
                                  double* __restrict__ on, double* __restrict__ oc, int64_t n_slots,
                                  int64_t slot_base, const int32_t* __restrict__ pool,
                                  const int32_t* __restrict__ pool_offset, const int32_t* __restrict__ pool_size,
