@@ -307,8 +307,11 @@ __device__ inline int warp_first_set(const uint32_t* words, int nw) {
 // and repeated pairs, 3 io rows + Kahn, 4 pruning + TC eligibility, 5 steps /
 // groups / slots; the full kernel adds the program writes) --
 // tools/time_transform.py times the cumulative phases
+#ifndef TNEAT_TR_WPB
+#define TNEAT_TR_WPB 1  // one genome-warp per CTA: its shared memory is released as soon as it finishes
+#endif
 template <typename T, bool SMALL>
-__global__ void __launch_bounds__(32, SMALL ? 24 : 1) transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
+__global__ void __launch_bounds__(32 * TNEAT_TR_WPB, SMALL ? 24 / TNEAT_TR_WPB : 1) transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
                                  int64_t P, int N, int C, int I, int O, int mode, int prune, bool tc,
                                  int64_t wsmem, uint8_t* __restrict__ prog, ProgLayout L,
                                  int16_t* __restrict__ order_out, int16_t* __restrict__ conn_rows,
@@ -1128,9 +1131,6 @@ int an_transform(const double* nodes, const double* conns, int64_t P, int N, int
   const int Cc = C > 0 ? C : 1;
   const int64_t ws = warp_smem_bytes(N, Cc, I);
   if (ws > 200 * 1024) return -4;  // genome capacity too large for one warp's shared memory
-#ifndef TNEAT_TR_WPB
-#define TNEAT_TR_WPB 1  // one genome-warp per CTA: its shared memory is released as soon as it finishes
-#endif
   int wpb = TNEAT_TR_WPB;
   while (wpb > 1 && ws * wpb > 160 * 1024) wpb >>= 1;
   const int64_t smem = ws * wpb;
