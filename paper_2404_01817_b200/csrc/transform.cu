@@ -310,8 +310,10 @@ __device__ inline int warp_first_set(const uint32_t* words, int nw) {
 #ifndef TNEAT_TR_WPB
 #define TNEAT_TR_WPB 1  // one genome-warp per CTA: its shared memory is released as soon as it finishes
 #endif
+// register bounds: fp32 small-key genomes are shared-memory-limited at 24 per
+// SM (80 registers); fp64 ones (small genomes, evolution) fit 32 at 62
 template <typename T, bool SMALL>
-__global__ void __launch_bounds__(32 * TNEAT_TR_WPB, SMALL ? 24 / TNEAT_TR_WPB : 1) transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
+__global__ void __launch_bounds__(32 * TNEAT_TR_WPB, SMALL ? (sizeof(T) == 8 ? 32 : 24) / TNEAT_TR_WPB : 1) transform_kernel(const double* __restrict__ nodes, const double* __restrict__ conns,
                                  int64_t P, int N, int C, int I, int O, int mode, int prune, bool tc,
                                  int64_t wsmem, uint8_t* __restrict__ prog, ProgLayout L,
                                  int16_t* __restrict__ order_out, int16_t* __restrict__ conn_rows,
